@@ -1,0 +1,123 @@
+"""O1: pairwise kernel functions and the plain direct sum (oracle; test infrastructure).
+
+Every kernel takes r = x - y (target minus source).
+Constants: Laplace 1/(4 pi), Stokes 1/(8 pi) with mu = 1
+(PAPER.md:251-253).
+
+Kernel names follow the paper's notation:
+  L          Laplace single layer, phi = q/(4 pi r)
+  L+gradL    [phi, grad_x phi], grad_x L = -r/(4 pi r^3)           PAPER.md:102-117, Table XI LapPGrad
+  G          Stokeslet (1/8pi)(delta/r + r r^T/r^3)
+  G_RPY      (1 + b^2/6 lap) G, Eq. (RPYkernel)
+  G_RPY+lapG [u, lap u]; lap G^RPY = lap G since lap lap G = 0
+  G+lapG     [u, lap u] from point forces                          PAPER.md:106, Table IV
+  G_eps      regularized Stokeslet
+with lap G_ij = (1/8pi)(2 delta_ij / r^3 - 6 r_i r_j / r^5) (derived from
+G_ij; checked by finite differences in tests/test_oracle_kernels.py).
+
+Singular kernels skip pairs with r^2 == 0 exactly (self interaction,
+DESIGN.md reading R5); G_eps is finite at r = 0 and keeps them.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+FOUR_PI = 4.0 * np.pi
+EIGHT_PI = 8.0 * np.pi
+
+# (k_s, k_t) of each named kernel
+DIMS = {
+    "L": (1, 1),
+    "L+gradL": (1, 4),
+    "G": (3, 3),
+    "G_RPY": (4, 3),
+    "G_RPY+lapG": (4, 6),
+    "G+lapG": (3, 6),
+    "G_eps": (4, 3),
+}
+SINGULAR = {"L": True, "L+gradL": True, "G": True, "G_RPY": True, "G_RPY+lapG": True,
+            "G+lapG": True, "G_eps": False}
+
+
+def pair_values(name: str, r: np.ndarray, s: np.ndarray) -> np.ndarray:
+    """Kernel `name` applied to source values s at displacement r = x - y.
+
+    r: (..., 3), s: (..., k_s) broadcastable -> (..., k_t).  Pairs with
+    r^2 == 0 contribute zero for singular kernels.
+    """
+    r2 = np.sum(r * r, axis=-1)
+    if name == "G_eps":
+        eps = s[..., 3]
+        f = s[..., :3]
+        d = r2 + eps * eps
+        d32 = d * np.sqrt(d)
+        rf = np.sum(r * f, axis=-1)
+        u = ((r2 + 2.0 * eps * eps)[..., None] * f + rf[..., None] * r) / d32[..., None]
+        return u / EIGHT_PI
+    zero = r2 == 0.0
+    r2s = np.where(zero, 1.0, r2)
+    rinv = 1.0 / np.sqrt(r2s)
+    rinv = np.where(zero, 0.0, rinv)
+    rinv3 = rinv * rinv * rinv
+    if name == "L":
+        return (s[..., 0] * rinv / FOUR_PI)[..., None]
+    if name == "L+gradL":
+        q = s[..., 0]
+        phi = q * rinv / FOUR_PI
+        grad = -(q * rinv3)[..., None] * r / FOUR_PI
+        return np.concatenate([phi[..., None], grad], axis=-1)
+    f = s[..., :3]
+    rf = np.sum(r * f, axis=-1)
+    if name == "G":
+        return (rinv[..., None] * f + (rf * rinv3)[..., None] * r) / EIGHT_PI
+    rinv5 = rinv3 * rinv * rinv
+    lap = (2.0 * rinv3[..., None] * f - 6.0 * (rf * rinv5)[..., None] * r) / EIGHT_PI
+    if name == "G+lapG":
+        u = (rinv[..., None] * f + (rf * rinv3)[..., None] * r) / EIGHT_PI
+        return np.concatenate([u, lap], axis=-1)
+    b2 = s[..., 3] * s[..., 3]
+    u = ((rinv + b2 * rinv3 / 3.0)[..., None] * f + ((rinv3 - b2 * rinv5) * rf)[..., None] * r) / EIGHT_PI
+    if name == "G_RPY":
+        return u
+    if name == "G_RPY+lapG":
+        return np.concatenate([u, lap], axis=-1)
+    raise ValueError(name)
+
+
+def direct_sum(name: str, trg: np.ndarray, src: np.ndarray, vals: np.ndarray,
+               chunk: int = 256) -> np.ndarray:
+    """Eq. (1)/(2): g(x_a) = sum_b K(x_a, y_b, s_b).
+
+    Plain all-pairs sum, chunked over targets only to bound memory.
+    """
+    k_t = DIMS[name][1]
+    trg = np.asarray(trg, dtype=np.float64)
+    src = np.asarray(src, dtype=np.float64)
+    vals = np.asarray(vals, dtype=np.float64)
+    out = np.zeros((trg.shape[0], k_t))
+    if src.shape[0] == 0:
+        return out
+    step = max(1, min(chunk, (1 << 24) // max(1, src.shape[0])))
+    for a in range(0, trg.shape[0], step):
+        r = trg[a:a + step, None, :] - src[None, :, :]
+        out[a:a + step] = pair_values(name, r, vals[None, :, :]).sum(axis=1)
+    return out
+
+
+def kernel_matrix(name: str, trg: np.ndarray, src: np.ndarray) -> np.ndarray:
+    """Dense matrix of a LINEAR ML-tree kernel (L or G): rows (i, a), cols (j, b).
+
+    Row index i*k + a (target point i, component a); column j*k + b.  Built by
+    applying the kernel to unit source vectors, i.e. straight from
+    pair_values, so the matrix and the pointwise kernel cannot disagree.
+    """
+    k = DIMS[name][0]
+    assert DIMS[name] == (k, k) and name in ("L", "G")
+    nt, ns = trg.shape[0], src.shape[0]
+    r = trg[:, None, :] - src[None, :, :]
+    K = np.empty((nt, k, ns, k))
+    for b in range(k):
+        e = np.zeros(k)
+        e[b] = 1.0
+        K[:, :, :, b] = np.moveaxis(pair_values(name, r, e), -1, 1)
+    return K.reshape(nt * k, ns * k)

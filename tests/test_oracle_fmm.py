@@ -1,0 +1,125 @@
+"""Pins for oracle/fmm.py (O2): the plain KIFMM against the direct sum and invariants.
+
+Parity of the FMM *approximation* itself is unpinned by the paper (it prints
+no numeric output); these tests pin what the mathematics fixes: degenerate
+trees equal the direct sum, linearity, convergence in p, exact covariance
+under scaling by 1/2 and under cube reflections/permutations, and agreement
+of the sampled mode with the full evaluation.
+"""
+import numpy as np
+import pytest
+
+import workloads as WL
+from oracle import fmm as F
+
+
+def _cloud(n, seed, kernel):
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, 3))
+    vals = WL.random_values(kernel, n, seed + 1)
+    return pts, vals
+
+
+@pytest.mark.parametrize("kernel", WL.KERNELS)
+def test_single_leaf_equals_direct(kernel):
+    pts, vals = _cloud(120, 1, kernel)
+    r = F.fmm(pts, vals, kernel, 4, 500)
+    assert r["tree"].nbox == 1
+    np.testing.assert_allclose(r["out"], F.direct(kernel, pts, vals), rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("kernel", WL.KERNELS)
+def test_zero_sources_and_superposition(kernel):
+    pts, v1 = _cloud(700, 2, kernel)
+    v2 = WL.random_values(kernel, 700, 99)
+    z = np.zeros_like(v1)
+    if v1.shape[1] == 4:
+        z[:, 3] = v1[:, 3]
+        v2[:, 3] = v1[:, 3]
+    assert np.all(F.fmm(pts, z, kernel, 4, 20)["out"] == 0.0)
+    a = F.fmm(pts, v1, kernel, 4, 20)["out"]
+    b = F.fmm(pts, v2, kernel, 4, 20)["out"]
+    s = v1 + 2 * v2
+    if v1.shape[1] == 4:
+        s[:, 3] = v1[:, 3]
+    c = F.fmm(pts, s, kernel, 4, 20)["out"]
+    np.testing.assert_allclose(c, a + 2 * b, rtol=0, atol=1e-12 * np.abs(c).max())
+
+
+@pytest.mark.parametrize("kernel,ps", [("laplace_pgrad", (4, 6, 8, 10)), ("stokeslet", (4, 6, 8))])
+def test_error_decreases_with_p(kernel, ps):
+    # PAPER.md:646 / :679 "as m linearly increases, the convergence error exponentially decreases"
+    pts, vals = _cloud(1500, 3, kernel)
+    d = F.direct(kernel, pts, vals)
+    errs = [F.rel_l2(F.fmm(pts, vals, kernel, p, 40)["out"], d) for p in ps]
+    for e0, e1 in zip(errs, errs[1:]):
+        assert e1 < e0 / 10.0, errs
+    assert errs[-1] < 1e-5
+
+
+def test_adaptive_tree_with_w_x_lists_matches_direct():
+    # clustered cloud forces W and X lists (adaptive); brute-force O1 comparison
+    rng = np.random.default_rng(11)
+    pts = np.concatenate([rng.random((150, 3)),
+                          np.clip(0.3 + 0.02 * rng.standard_normal((350, 3)), 0, 0.999)])
+    vals = WL.random_values("laplace_pgrad", 500, 12)
+    r = F.fmm(pts, vals, "laplace_pgrad", 10, 8, keep_internals=True)
+    assert sum(len(w) for w in r["W"].values()) > 0 and sum(len(x) for x in r["X"].values()) > 0
+    d = F.direct("laplace_pgrad", pts, vals)
+    for lo, hi in F.blocks("laplace_pgrad"):
+        assert F.rel_l2(r["out"][:, lo:hi], d[:, lo:hi]) < 1e-6
+
+
+def test_tiny_brute_force_p12_laplace():
+    rng = np.random.default_rng(5)
+    pts = rng.random((200, 3))
+    vals = WL.random_values("laplace_pgrad", 200, 6)
+    r = F.fmm(pts, vals, "laplace_pgrad", 12, 4)
+    assert r["tree"].depth >= 3
+    d = F.direct("laplace_pgrad", pts, vals)
+    assert F.rel_l2(r["out"][:, :1], d[:, :1]) < 1e-8
+
+
+@pytest.mark.parametrize("kernel", WL.KERNELS)
+def test_scale_covariance_is_exact(kernel):
+    # x -> x/2 moves the tree one level down; L and G are homogeneous of degree -1,
+    # grad L of degree -2, lap G of degree -3 (b, eps scale with x)
+    pts, vals = _cloud(900, 7, kernel)
+    a = F.fmm(pts, vals, kernel, 5, 30)["out"]
+    v2 = vals.copy()
+    if v2.shape[1] == 4:
+        v2[:, 3] *= 0.5
+    b = F.fmm(pts * 0.5, v2, kernel, 5, 30)["out"]
+    scale = {"laplace_pgrad": [2, 4, 4, 4], "stokeslet": [2] * 3, "rpy": [2] * 3 + [8] * 3,
+             "stokes_reg_vel": [2] * 3}[kernel]
+    np.testing.assert_allclose(b, a * np.array(scale, float), rtol=0, atol=1e-13 * np.abs(b).max())
+
+
+@pytest.mark.parametrize("kernel", ["stokeslet", "rpy"])
+def test_cube_symmetry_covariance(kernel):
+    # reflection x_0 -> 1 - x_0 composed with the axis swap (x_1 <-> x_2)
+    pts, vals = _cloud(900, 8, kernel)
+    R = np.array([[-1, 0, 0], [0, 0, 1], [0, 1, 0]], float)
+    p2 = pts @ R.T
+    p2[:, 0] += 1.0
+    p2 = np.where(p2 >= 1.0, np.nextafter(1.0, 0.0), p2)
+    v2 = vals.copy()
+    v2[:, :3] = vals[:, :3] @ R.T
+    a = F.fmm(pts, vals, kernel, 6, 30)["out"]
+    b = F.fmm(p2, v2, kernel, 6, 30)["out"]
+    ra = a.copy()
+    ra[:, :3] = a[:, :3] @ R.T
+    if a.shape[1] == 6:
+        ra[:, 3:] = a[:, 3:] @ R.T
+    # SVD factors are equivariant only up to rounding amplified by 1/sigma_min (~1e-11)
+    assert F.rel_l2(b, ra) < 1e-10
+
+
+@pytest.mark.parametrize("kernel", WL.KERNELS)
+def test_sampled_mode_equals_full(kernel):
+    pts, vals = _cloud(1200, 9, kernel)
+    full = F.fmm(pts, vals, kernel, 5, 25)
+    t = full["tree"]
+    leaves = F.sample_leaves(t, 150, seed=4)
+    s = F.fmm(pts, vals, kernel, 5, 25, target_leaves=leaves, tree=t)
+    np.testing.assert_allclose(s["out"], full["out"][s["idx"]], rtol=0, atol=1e-13 * np.abs(s["out"]).max())

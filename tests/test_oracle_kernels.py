@@ -1,0 +1,200 @@
+"""Pins for oracle/kernels.py (O1): closed forms, identities, special cases.
+
+None of these re-types the oracle's formula: each checks it against a
+different fact (a hand-worked value, a finite-difference derivative, the
+defining equation of a derived kernel, a symmetry or a limit).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle.kernels import DIMS, direct_sum, kernel_matrix, pair_values
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "kernel_values.txt")
+
+
+def _golden_rows():
+    rows = []
+    for line in open(GOLD):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        name, r, s, g, cite = [p.strip() for p in line.split("|")]
+        rows.append((name, np.array(r.split(), float), np.array(s.split(), float),
+                     np.array(g.split(), float), cite))
+    return rows
+
+
+@pytest.mark.parametrize("row", _golden_rows(), ids=lambda r: f"{r[0]}@{r[4]}")
+def test_golden_closed_form(row):
+    name, r, s, g, _ = row
+    out = pair_values(name, r, s)
+    np.testing.assert_allclose(out, g, rtol=1e-15, atol=1e-17)
+
+
+def _fd_grad(f, x, h):
+    """4th-order central differences of a vector function along each axis."""
+    cols = []
+    for a in range(3):
+        e = np.zeros(3)
+        e[a] = h
+        cols.append((-f(x + 2 * e) + 8 * f(x + e) - 8 * f(x - e) + f(x - 2 * e)) / (12 * h))
+    return np.stack(cols, axis=-1)  # (..., comp, axis)
+
+
+def _fd_lap(f, x, h):
+    acc = 0.0
+    for a in range(3):
+        e = np.zeros(3)
+        e[a] = h
+        acc = acc + (-f(x + 2 * e) + 16 * f(x + e) - 30 * f(x) + 16 * f(x - e) - f(x - 2 * e)) / (12 * h * h)
+    return acc
+
+
+RNG = np.random.default_rng(7)
+RS = [RNG.standard_normal(3) * s for s in (0.3, 1.0, 3.0)]
+
+
+@pytest.mark.parametrize("r", RS)
+def test_laplace_gradient_is_grad_of_potential(r):
+    # grad_x phi with the sign rule d/dx = -d/dy
+    q = np.array([1.7])
+    phi = lambda x: pair_values("L", x, q)
+    fd = _fd_grad(phi, r, 1e-4 * max(np.linalg.norm(r), 1))[0]
+    an = pair_values("L+gradL", r, q)
+    np.testing.assert_allclose(an[0], phi(r)[0], rtol=1e-15)
+    np.testing.assert_allclose(an[1:], fd, rtol=1e-6)
+
+
+@pytest.mark.parametrize("r", RS)
+def test_stokeslet_divergence_free_and_symmetric(r):
+    h = 1e-3 * np.linalg.norm(r)
+    for b in range(3):
+        f = np.zeros(3)
+        f[b] = 1.0
+        J = _fd_grad(lambda x: pair_values("G", x, f), r, h)
+        assert abs(np.trace(J)) < 1e-7 * np.abs(J).max()
+    K = kernel_matrix("G", r[None, :], np.zeros((1, 3)))
+    np.testing.assert_allclose(K, K.T, rtol=0, atol=1e-16)
+    K2 = kernel_matrix("G", -r[None, :], np.zeros((1, 3)))
+    np.testing.assert_allclose(K, K2, rtol=1e-15)
+
+
+@pytest.mark.parametrize("r", RS)
+def test_lapG_is_laplacian_of_stokeslet_and_biharmonic(r):
+    f = np.array([0.3, -1.1, 0.8])
+    h = 1e-3 * np.linalg.norm(r)
+    u = lambda x: pair_values("G", x, f)
+    lap_fd = _fd_lap(u, r, h)
+    lap = pair_values("G+lapG", r, f)[3:]
+    np.testing.assert_allclose(lap, lap_fd, rtol=1e-6 * 1e3, atol=1e-6 * np.abs(lap).max())
+    # lap lap G = 0: Laplacian of the analytic lap G vanishes
+    bih = _fd_lap(lambda x: pair_values("G+lapG", x, f)[..., 3:], r, h)
+    assert np.abs(bih).max() < 1e-5 * np.abs(lap).max() / np.dot(r, r)
+
+
+@pytest.mark.parametrize("r", RS)
+def test_rpy_is_one_plus_b2_over_6_lap_on_G(r):
+    # Eq. (RPYkernel): G^RPY = (1 + b^2/6 lap) G, lap G by finite differences
+    f = np.array([0.3, -1.1, 0.8])
+    b = 0.2 * np.linalg.norm(r)
+    u = lambda x: pair_values("G", x, f)
+    expect = u(r) + b * b / 6.0 * _fd_lap(u, r, 1e-3 * np.linalg.norm(r))
+    got = pair_values("G_RPY", r, np.r_[f, b])
+    np.testing.assert_allclose(got, expect, rtol=1e-7)
+
+
+def test_rpy_special_cases():
+    rng = np.random.default_rng(3)
+    r = rng.standard_normal((50, 3))
+    f = rng.standard_normal((50, 3))
+    g = pair_values("G", r, f)
+    # b = 0 reduces exactly to the Stokeslet
+    np.testing.assert_array_equal(pair_values("G_RPY", r, np.c_[f, np.zeros(50)]), g)
+    # lap u is independent of b (lap lap G = 0)
+    a1 = pair_values("G_RPY+lapG", r, np.c_[f, np.full(50, 0.01)])
+    a2 = pair_values("G_RPY+lapG", r, np.c_[f, np.full(50, 0.3)])
+    np.testing.assert_array_equal(a1[:, 3:], a2[:, 3:])
+    np.testing.assert_array_equal(a1[:, 3:], pair_values("G+lapG", r, f)[:, 3:])
+    # far field -> Stokeslet, difference O(b^2/r^2)
+    rr = r * 100.0
+    d = pair_values("G_RPY", rr, np.c_[f, np.full(50, 0.01)]) - pair_values("G", rr, f)
+    assert np.abs(d).max() < 1e-7 * np.abs(pair_values("G", rr, f)).max()
+
+
+def test_regularized_stokeslet_limits():
+    rng = np.random.default_rng(4)
+    r = rng.standard_normal((50, 3))
+    f = rng.standard_normal((50, 3))
+    # eps = 0 -> the singular Stokeslet (r != 0)
+    np.testing.assert_allclose(pair_values("G_eps", r, np.c_[f, np.zeros(50)]),
+                               pair_values("G", r, f), rtol=1e-14)
+    # G^eps - G^RPY(b^2 = 1.5 eps^2) = O((eps/r)^4)
+    rr = r / np.linalg.norm(r, axis=1, keepdims=True)
+    errs = []
+    for eps in (1e-1, 5e-2):
+        d = pair_values("G_eps", rr, np.c_[f, np.full(50, eps)]) - pair_values(
+            "G_RPY", rr, np.c_[f, np.full(50, np.sqrt(1.5) * eps)])
+        errs.append(np.abs(d).max())
+    assert 12.0 < errs[0] / errs[1] < 20.0  # fourth order: 2^4 = 16
+
+
+def test_regularized_stokeslet_divergence_free_and_blob_mass():
+    # incompressible regularized flow: div(G^eps f) = 0
+    r = np.array([0.02, -0.01, 0.015])
+    f = np.array([0.3, -1.1, 0.8])
+    J = _fd_grad(lambda x: pair_values("G_eps", x, np.r_[f, 0.01]), r, 1e-4)
+    assert abs(np.trace(J)) < 1e-7 * np.abs(J).max()
+    # blob psi^eps integrates to 1: radial quadrature
+    eps = 0.3
+    from scipy.integrate import quad
+    val, _ = quad(lambda s: 4 * np.pi * s * s * 15 * eps ** 4 / (8 * np.pi * (s * s + eps * eps) ** 3.5), 0, np.inf)
+    assert abs(val - 1.0) < 1e-10
+
+
+def test_self_pairs_skipped_for_singular_kept_for_regularized():
+    z = np.zeros(3)
+    for name in ("L", "L+gradL", "G", "G_RPY", "G_RPY+lapG", "G+lapG"):
+        s = np.ones(DIMS[name][0])
+        assert np.all(pair_values(name, z, s) == 0.0)
+    assert np.all(pair_values("G_eps", z, np.array([1.0, 0, 0, 0.1]))[0] > 0)
+
+
+def test_direct_sum_superposition_permutation_reciprocity():
+    rng = np.random.default_rng(5)
+    y = rng.random((300, 3))
+    f1 = rng.standard_normal((300, 3))
+    f2 = rng.standard_normal((300, 3))
+    a = direct_sum("G", y, y, f1)
+    b = direct_sum("G", y, y, f2)
+    np.testing.assert_allclose(direct_sum("G", y, y, f1 + 2 * f2), a + 2 * b, rtol=1e-12, atol=1e-12)
+    perm = rng.permutation(300)
+    np.testing.assert_allclose(direct_sum("G", y[perm], y[perm], f1[perm]), a[perm], rtol=1e-12)
+    # reciprocity of the symmetric mobility: f1 . (M f2) = f2 . (M f1)
+    assert abs(np.sum(f1 * b) - np.sum(f2 * a)) < 1e-11 * abs(np.sum(f1 * b))
+    # same for RPY (symmetric positive definite mobility)
+    v1 = np.c_[f1, np.full(300, 1e-3)]
+    v2 = np.c_[f2, np.full(300, 1e-3)]
+    ra = direct_sum("G_RPY", y, y, v1)
+    rb = direct_sum("G_RPY", y, y, v2)
+    assert abs(np.sum(f1 * rb) - np.sum(f2 * ra)) < 1e-11 * abs(np.sum(f1 * rb))
+
+
+def test_direct_sum_two_opposite_charges_and_scalar_loop():
+    y = np.array([[0.2, 0.5, 0.5], [0.8, 0.5, 0.5]])
+    q = np.array([[1.0], [-1.0]])
+    x = np.array([[0.5, 0.1, 0.9], [0.5, 0.7, 0.3]])   # on the bisecting plane
+    assert np.all(np.abs(direct_sum("L", x, y, q)) < 1e-16)
+    # scalar double loop over pairs (no broadcasting) agrees with the vectorised sum
+    rng = np.random.default_rng(8)
+    X = rng.random((7, 3))
+    Y = np.r_[rng.random((9, 3)), X[:2]]
+    V = np.c_[rng.standard_normal((11, 3)), np.full(11, 0.05)]
+    for name in ("G_RPY+lapG", "G_eps", "L+gradL"):
+        vv = V[:, : DIMS[name][0]]
+        ref = np.zeros((7, DIMS[name][1]))
+        for i in range(7):
+            for j in range(11):
+                ref[i] += pair_values(name, X[i] - Y[j], vv[j])
+        np.testing.assert_allclose(direct_sum(name, X, Y, vv), ref, rtol=1e-13, atol=1e-13)

@@ -1,0 +1,129 @@
+"""Pins for oracle/operators.py: surfaces, SVD factors, composed and raw operators."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import operators as O
+from oracle.kernels import direct_sum, kernel_matrix
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "surface_counts.txt")
+
+
+def test_surface_counts_golden():
+    for line in open(GOLD):
+        if line.startswith("#") or not line.strip():
+            continue
+        m, M = map(int, line.split())
+        assert len(O.surface_lattice(m)) == M == O.n_surface(m)
+    for m in range(2, 17):
+        assert len(O.surface_lattice(m)) == m ** 3 - max(m - 2, 0) ** 3
+
+
+def test_surface_geometry():
+    s = O.surface(8, [0.25, 0.5, 0.75], 0.125, 2.95)
+    d = np.abs(s - np.array([0.25, 0.5, 0.75]))
+    assert np.allclose(d.max(axis=1), 2.95 * 0.125)      # on the cube boundary
+    assert len(np.unique(np.round(s, 12), axis=0)) == 296  # no duplicates at edges/corners
+    assert O.surface(2, [0, 0, 0], 1.0, 1.0).shape == (8, 3)
+
+
+@pytest.fixture(scope="module")
+def lap8():
+    return O.Operators("L", 8)
+
+
+@pytest.fixture(scope="module")
+def stk6():
+    return O.Operators("G", 6)
+
+
+def test_kept_counts_laplace_p10():
+    op = O.Operators("L", 10)
+    assert op.up_kept == op.dn_kept == 426   # SURVEY.md §8(c) R2 (tau = 1e-12)
+
+
+def test_kept_counts_stokeslet_p8():
+    op = O.Operators("G", 8)
+    assert op.up_kept == op.dn_kept == 875
+    s = op.up_sigma / op.up_sigma[0]
+    # the threshold sits >= 1.4% (0.006 dex) away from every singular value
+    assert np.min(np.abs(np.log10(s) - np.log10(O.TAU))) > 0.006
+
+
+@pytest.mark.parametrize("fx", ["lap8", "stk6"])
+def test_check_to_equivalent_round_trip(fx, request):
+    op = request.getfixturevalue(fx)
+    rng = np.random.default_rng(1)
+    K = kernel_matrix(op.ml, O.surface(op.m, O.C0, O.H0, O.ALPHA_UC), O.surface(op.m, O.C0, O.H0, O.ALPHA_UE))
+    chk = K @ rng.standard_normal(op.n)
+    back = K @ op.uc2ue(chk, 0)
+    assert np.linalg.norm(back - chk) / np.linalg.norm(chk) < 1e-10
+
+
+@pytest.mark.parametrize("ml,name,k", [("L", "L", 1), ("G", "G", 3)])
+def test_single_box_far_field_equivalence_converges(ml, name, k):
+    # S->M of random interior sources reproduces the far field; error falls with m
+    rng = np.random.default_rng(2)
+    src = O.C0 + O.H0 * (2 * rng.random((40, 3)) - 1)
+    val = rng.standard_normal((40, k))
+    far = O.C0 + np.array([3.0, 0.4, -0.2]) * 2 * O.H0 + 0.3 * rng.standard_normal((30, 3))
+    ref = direct_sum(name, far, src, val)
+    errs = []
+    for m in (4, 6, 8):
+        op = O.Operators(ml, m)
+        chk = direct_sum(name, O.surface(m, O.C0, O.H0, O.ALPHA_UC), src, val).reshape(-1)
+        ue = op.uc2ue(chk, 0).reshape(-1, k)
+        got = direct_sum(name, far, O.surface(m, O.C0, O.H0, O.ALPHA_UE), ue)
+        errs.append(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    assert errs[0] > 10 * errs[1] > 100 * errs[2]
+    assert errs[2] < 1e-5
+
+
+def test_level_scaling_is_exact(lap8):
+    # homogeneity of degree -1: level-3 geometry = 2^3 x level-0 matrix
+    h3 = O.H0 / 8
+    c3 = np.array([0.3125, 0.5625, 0.1875])
+    K3 = kernel_matrix("L", O.surface(8, c3, h3, O.ALPHA_DC), O.surface(8, c3 + 2 * h3 * np.array([2, -3, 1]), h3, O.ALPHA_UE))
+    K0 = lap8.m2l_matrix((2, -3, 1))
+    np.testing.assert_allclose(K3, 8.0 * K0, rtol=1e-13)
+
+
+def test_m2l_mirror_symmetry(stk6):
+    # M2L[-o] = P M2L[o] P^T with P the point reflection of the lattice (G(-r) = G(r))
+    lat = O.surface_lattice(6)
+    key = {tuple(v): i for i, v in enumerate(lat)}
+    perm = np.array([key[tuple(5 - v)] for v in lat])
+    P = np.kron(np.eye(len(lat))[perm], np.eye(3))
+    A = stk6.m2l_matrix((2, 1, -3))
+    B = stk6.m2l_matrix((-2, -1, 3))
+    np.testing.assert_allclose(P @ A @ P.T, B, rtol=1e-13, atol=1e-13 * np.abs(A).max())
+
+
+def test_composed_m2m_and_l2l_match_two_step(lap8):
+    # Equivalent densities are fixed only up to near-null modes of the SVD, so the
+    # two routes are compared through the fields they generate (outside the parent
+    # for M2M, inside the child for L2L), which is what the method matches.
+    rng = np.random.default_rng(3)
+    far = O.C0 + np.array([4.0, 1.0, -2.0]) * O.H0 + 0.5 * O.H0 * rng.standard_normal((40, 3))
+    ue_p = O.surface(8, O.C0, O.H0, O.ALPHA_UE)
+    for o in (0, 5, 7):
+        cc = O.C0 + 0.5 * O.H0 * O.child_centre_offset(o)
+        ue_c = rng.standard_normal(lap8.n)
+        chk = kernel_matrix("L", O.surface(8, O.C0, O.H0, O.ALPHA_UC), O.surface(8, cc, O.H0 / 2, O.ALPHA_UE)) @ ue_c
+        a = direct_sum("L", far, ue_p, (lap8.m2m[o] @ ue_c)[:, None])
+        b = direct_sum("L", far, ue_p, lap8.uc2ue(chk, 0)[:, None])
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-11
+        de_p = rng.standard_normal(lap8.n)
+        inside = cc + 0.5 * O.H0 * (2 * rng.random((40, 3)) - 1)
+        chk = kernel_matrix("L", O.surface(8, cc, O.H0 / 2, O.ALPHA_DC), O.surface(8, O.C0, O.H0, O.ALPHA_DE)) @ de_p
+        de_c = O.surface(8, cc, O.H0 / 2, O.ALPHA_DE)
+        a = direct_sum("L", inside, de_c, (lap8.l2l[o] @ de_p)[:, None])
+        b = direct_sum("L", inside, de_c, lap8.dc2de(chk, 1)[:, None])
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-11
+
+
+def test_v_offsets():
+    offs = O.v_offsets()
+    assert len(offs) == 316 and len(set(offs)) == 316
+    assert all(max(map(abs, o)) in (2, 3) for o in offs)
