@@ -1,0 +1,158 @@
+/*
+ * kafmm.h -- C ABI of the B200-native Kernel Aggregated FMM evaluation pass.
+ *
+ * Method: Yan & Blackwell, "Kernel Aggregated Fast Multipole Method",
+ * arXiv 2010.15155.  The library approximates the kernel sum
+ *     g_i(x^a) = sum_b K_ij(x^a, y^b, s^b)                 Eq. (1)/(2)
+ * with a kernel-independent FMM whose eight traversal stages use the kernels
+ * of the paper's kernel tables (Table I; Tables IV/V,
+ * PAPER.md:292-349): the ML-tree stages (M2M, M2L, L2L) use the linear
+ * Laplace kernel L or Stokeslet G, the S-row the (possibly nonlinear)
+ * source kernel, the T-column the target kernel.
+ *
+ * Sources and targets are the same point set.
+ *
+ * Memory: every pointer argument named "device" is a CUDA device pointer on
+ * the current device with 8-byte alignment (e.g. torch.Tensor.data_ptr());
+ * arrays are row-major, C-contiguous float64.  The caller owns its arrays; the
+ * plan owns every tree, list, operator and workspace buffer until
+ * kafmm_destroy().  kafmm_setup copies the points, so they may be freed on
+ * return.  No exception ever crosses this ABI: every entry point returns a
+ * status; the detail string of the last failure on the calling thread is
+ * kafmm_last_error().
+ *
+ * There is no CPU fallback: without a CUDA device every entry point that
+ * computes returns KAFMM_ECUDA.
+ */
+#ifndef KAFMM_H
+#define KAFMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kafmm_plan_s* kafmm_plan; /* opaque; owned by the library */
+
+typedef enum {
+  KAFMM_OK = 0,
+  KAFMM_EINVAL = 1,     /* null pointer, n < 1, p < 2, max_pts < 1, unknown kernel */
+  KAFMM_EDOMAIN = 2,    /* a point outside [0,1)^3 */
+  KAFMM_ENONFINITE = 3, /* NaN/Inf in points or values, or negative b / eps */
+  KAFMM_ENOMEM = 4,     /* device allocation failed */
+  KAFMM_ECUDA = 5,      /* CUDA / cuBLAS / cuSOLVER error (detail in kafmm_last_error) */
+  KAFMM_ENCCL = 6,      /* reserved: multi-GPU exchange error */
+  KAFMM_ESTATE = 7      /* invalid plan state */
+} kafmm_status;
+
+/* Kernel summation problems (Table XI).
+ *   LAPLACE_PGRAD   k_s=1 [q]        k_t=4 [phi, dphi/dx, dphi/dy, dphi/dz]
+ *                   phi = sum q/(4 pi r), grad w.r.t. the target
+ *   STOKESLET       k_s=3 [f]        k_t=3 [u], u = sum G f
+ *   RPY             k_s=4 [f, b]     k_t=6 [u, lap u], u = sum G^RPY(b) f, lap u = sum lap G f
+ *                   (Eqs. RPYflow/RPYkernel, Table IV); the target
+ *                   radius assembly u + a^2/6 lap u (Eq. RPYtrgvel) is the caller's
+ *   STOKES_REG_VEL  k_s=4 [f, eps]   k_t=3 [u], u = sum G^eps f
+ * Self pairs (r^2 == 0) are skipped by the singular kernels and kept by
+ * STOKES_REG_VEL, where G^eps(0) = 1/(4 pi eps) is finite. */
+typedef enum {
+  KAFMM_LAPLACE_PGRAD = 1,
+  KAFMM_STOKESLET = 2,
+  KAFMM_RPY = 3,
+  KAFMM_STOKES_REG_VEL = 4
+} kafmm_kernel;
+
+/* Source and target dimensions of a kernel.  EINVAL for an unknown kernel. */
+kafmm_status kafmm_kernel_dims(int kernel, int* k_s, int* k_t);
+
+/* Build the plan: Morton-sort the points, build the adaptive octree (a box
+ * splits iff it holds more than max_pts_per_leaf points and its level < 20),
+ * the U/V/W/X lists and the translation operators at
+ * multipole order p (M = 6(p-1)^2+2 surface points).
+ *   points            device, n x 3 (x, y, z), every coordinate in [0, 1)
+ *   n                 number of points (>= 1)
+ *   kernel            a kafmm_kernel value
+ *   p                 multipole order m of the paper, >= 2
+ *   max_pts_per_leaf  leaf capacity, >= 1
+ *   out               receives the plan (NULL on failure)
+ * Synchronous: returns after the plan is complete. */
+kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p,
+                         int max_pts_per_leaf, kafmm_plan* out);
+
+/* Stream for subsequent kafmm_eval calls (default: the legacy default stream).
+ * `stream` is a cudaStream_t passed as void*. */
+kafmm_status kafmm_set_stream(kafmm_plan plan, void* stream);
+
+/* One evaluation pass (the hot path): S2M, UC2UE, M2M, M2L, S2L, DC2DE, L2L,
+ * L2T, M2T and P2P, then un-permute to user order.
+ *   src_values  device, n x k_s, user (setup) order
+ *   trg_out     device, n x k_t, user order, overwritten
+ * Asynchronous on the plan's stream; trg_out is valid after stream sync.
+ * A plan serves one evaluation at a time (single workspace). */
+kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_out);
+
+/* End-to-end variant with HOST buffers: copies src_values host->device, runs
+ * kafmm_eval and copies trg_out device->host, then synchronises the stream.
+ *   src_values  host, n x k_s (pinned memory gives full copy bandwidth)
+ *   trg_out     host, n x k_t */
+kafmm_status kafmm_eval_host(kafmm_plan plan, const double* src_values, double* trg_out);
+
+/* Validate source values (finite; b / eps >= 0) on the device.  Synchronous.
+ * kafmm_eval itself does not check, to keep the hot path free of host syncs. */
+kafmm_status kafmm_check_values(kafmm_plan plan, const double* src_values);
+
+/* Waits for the plan's stream; surfaces asynchronous CUDA errors. */
+kafmm_status kafmm_sync(kafmm_plan plan);
+
+void kafmm_destroy(kafmm_plan plan);
+
+const char* kafmm_status_string(int status);
+const char* kafmm_last_error(void);
+
+/* ---- introspection (tests, bench) ------------------------------------- */
+typedef struct {
+  int64_t n_points;
+  int kernel, p, max_pts, depth;
+  int k_s, k_t;
+  int n_surf;           /* M = 6(p-1)^2 + 2 */
+  int n_equiv;          /* n = k * M, length of one equivalent/check vector */
+  int kept_up, kept_dn; /* singular values kept by UC2UE / DC2DE (tau = 1e-12) */
+  int64_t n_boxes, n_leaves;
+  int64_t n_u_pairs;    /* (target leaf, source leaf) U-list entries */
+  int64_t n_v_pairs;    /* M2L (target box, source box) pairs */
+  int64_t n_w_pairs;    /* M2T pairs == S2L (X-list) pairs */
+  int64_t n_p2p;        /* point-point interactions in P2P */
+  int64_t workspace_bytes;
+} kafmm_info;
+
+kafmm_status kafmm_get_info(kafmm_plan plan, kafmm_info* info);
+
+/* Copy the octree to HOST arrays of length info.n_boxes (any may be NULL):
+ * level, ijk (n_boxes x 3, integer coords at the box's level), parent (-1 for
+ * root), is_leaf (0/1), pt_begin/pt_end (range in Morton order). Boxes are
+ * ordered by level, then Morton key. */
+kafmm_status kafmm_get_tree(kafmm_plan plan, int32_t* level, int32_t* ijk, int32_t* parent,
+                            int32_t* is_leaf, int64_t* pt_begin, int64_t* pt_end);
+
+/* HOST array of length n: perm[i] = user index of the i-th point in Morton order. */
+kafmm_status kafmm_get_permutation(kafmm_plan plan, int64_t* perm);
+
+/* Interaction lists as HOST pair arrays (target box, source box), lengths from
+ * kafmm_get_info: which = 'U' (n_u_pairs), 'V' (n_v_pairs), 'W' (n_w_pairs:
+ * target leaf, source box), 'X' (n_w_pairs: target box, source leaf). */
+kafmm_status kafmm_get_list(kafmm_plan plan, int which, int32_t* tgt, int32_t* src);
+
+/* Per-stage device times (ms) of the most recent kafmm_eval when stage
+ * timing is on (kafmm_set_timing(plan, 1)); names via kafmm_stage_name. */
+#define KAFMM_N_STAGES 12
+kafmm_status kafmm_set_timing(kafmm_plan plan, int on);
+kafmm_status kafmm_stage_times(kafmm_plan plan, float* ms /* KAFMM_N_STAGES */);
+const char* kafmm_stage_name(int stage);
+/* Kernel launches issued by one kafmm_eval. */
+kafmm_status kafmm_launch_count(kafmm_plan plan, int* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KAFMM_H */

@@ -1,0 +1,307 @@
+// extern "C" boundary of libkafmm.so (include/kafmm.h).  Every entry point
+// catches internal errors and turns them into a kafmm_status; the detail
+// string is kept per thread for kafmm_last_error().
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "kafmm_internal.h"
+
+namespace kafmm {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+static int dims(int kernel, int* ks, int* kt) {
+  switch (kernel) {
+    case KAFMM_LAPLACE_PGRAD: *ks = 1; *kt = 4; return 0;
+    case KAFMM_STOKESLET: *ks = 3; *kt = 3; return 0;
+    case KAFMM_RPY: *ks = 4; *kt = 6; return 0;
+    case KAFMM_STOKES_REG_VEL: *ks = 4; *kt = 3; return 0;
+    default: return -1;
+  }
+}
+
+static void free_plan(kafmm_plan_s* P) {
+  if (!P) return;
+  cudaStreamSynchronize(P->stream);
+  for (void* p : P->allocs) cudaFree(p);
+  for (auto& e : P->ev)
+    if (e) cudaEventDestroy(e);
+  delete P;
+}
+}  // namespace kafmm
+
+using namespace kafmm;
+
+#define KF_API_BEGIN try {
+#define KF_API_END                                 \
+  }                                                \
+  catch (const Error& e) {                         \
+    set_error(e.msg);                              \
+    return e.st;                                   \
+  }                                                \
+  catch (const std::bad_alloc&) {                  \
+    set_error("host allocation failed");           \
+    return KAFMM_ENOMEM;                           \
+  }                                                \
+  catch (...) {                                    \
+    set_error("unknown internal error");           \
+    return KAFMM_ECUDA;                            \
+  }
+
+extern "C" {
+
+kafmm_status kafmm_kernel_dims(int kernel, int* k_s, int* k_t) {
+  int a, b;
+  if (dims(kernel, &a, &b) != 0) {
+    set_error("unknown kernel");
+    return KAFMM_EINVAL;
+  }
+  if (k_s) *k_s = a;
+  if (k_t) *k_t = b;
+  return KAFMM_OK;
+}
+
+kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int max_pts_per_leaf,
+                         kafmm_plan* out) {
+  if (out) *out = nullptr;
+  int ks, kt;
+  if (!points || !out || n < 1 || p < 2 || max_pts_per_leaf < 1 || dims(kernel, &ks, &kt) != 0) {
+    set_error("kafmm_setup: invalid argument");
+    return KAFMM_EINVAL;
+  }
+  kafmm_plan_s* P = nullptr;
+  KF_API_BEGIN
+  int dev = 0;
+  KF_CUDA(cudaGetDevice(&dev));
+  P = new kafmm_plan_s();
+  P->kernel = kernel;
+  P->p = p;
+  P->cap = max_pts_per_leaf;
+  P->n = n;
+  P->ks = ks;
+  P->kt = kt;
+  P->kml = (kernel == KAFMM_LAPLACE_PGRAD) ? 1 : 3;
+  P->srec = (kernel == KAFMM_LAPLACE_PGRAD) ? 4 : 8;
+  P->M = 6 * (p - 1) * (p - 1) + 2;
+  P->neq = P->kml * P->M;
+  P->ldn = round_up(P->neq, GEMM_BK);
+  P->stream = 0;
+  build_tree_and_lists(*P, points);
+  build_operators(*P);
+  build_gemm_batches(*P);
+  P->d_rec = dalloc<double>(*P, (size_t)n * P->srec);
+  P->d_outs = dalloc<double>(*P, (size_t)n * kt);
+  P->d_ue = dalloc<double>(*P, (size_t)P->nbox * P->ldn);
+  P->d_chk = dalloc<double>(*P, (size_t)P->nbox * P->ldn);
+  P->d_de = dalloc<double>(*P, (size_t)P->nbox * P->ldn);
+  P->d_t = dalloc<double>(*P, (size_t)P->nbox * P->ldk);
+  for (auto& e : P->ev) KF_CUDA(cudaEventCreate(&e));
+  KF_CUDA(cudaStreamSynchronize(P->stream));
+  *out = P;
+  return KAFMM_OK;
+  }
+  catch (const Error& e) {
+    set_error(e.msg);
+    free_plan(P);
+    cudaGetLastError();
+    return e.st;
+  }
+  catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    free_plan(P);
+    return KAFMM_ENOMEM;
+  }
+}
+
+kafmm_status kafmm_set_stream(kafmm_plan plan, void* stream) {
+  if (!plan) return KAFMM_EINVAL;
+  plan->stream = (cudaStream_t)stream;
+  return KAFMM_OK;
+}
+
+kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_out) {
+  if (!plan || !src_values || !trg_out) {
+    set_error("kafmm_eval: null argument");
+    return KAFMM_EINVAL;
+  }
+  KF_API_BEGIN
+  run_eval(*plan, src_values, trg_out);
+  if (plan->timing) {
+    KF_CUDA(cudaEventSynchronize(plan->ev[ST_TOTAL]));
+    for (int s = 0; s < ST_TOTAL; ++s) KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[s], plan->ev[s], plan->ev[s + 1]));
+    KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[ST_TOTAL], plan->ev[0], plan->ev[ST_TOTAL]));
+  }
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_eval_host(kafmm_plan plan, const double* src_values, double* trg_out) {
+  if (!plan || !src_values || !trg_out) {
+    set_error("kafmm_eval_host: null argument");
+    return KAFMM_EINVAL;
+  }
+  KF_API_BEGIN
+  Plan& P = *plan;
+  if (!P.d_stage_in) {
+    P.d_stage_in = dalloc<double>(P, (size_t)P.n * P.ks);
+    P.d_stage_out = dalloc<double>(P, (size_t)P.n * P.kt);
+  }
+  KF_CUDA(cudaMemcpyAsync(P.d_stage_in, src_values, (size_t)P.n * P.ks * 8, cudaMemcpyHostToDevice, P.stream));
+  run_eval(P, P.d_stage_in, P.d_stage_out);
+  KF_CUDA(cudaMemcpyAsync(trg_out, P.d_stage_out, (size_t)P.n * P.kt * 8, cudaMemcpyDeviceToHost, P.stream));
+  KF_CUDA(cudaStreamSynchronize(P.stream));
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_check_values(kafmm_plan plan, const double* src_values) {
+  if (!plan || !src_values) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  check_values(*plan, src_values);
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_sync(kafmm_plan plan) {
+  if (!plan) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  KF_CUDA(cudaStreamSynchronize(plan->stream));
+  KF_CUDA(cudaGetLastError());
+  return KAFMM_OK;
+  KF_API_END
+}
+
+void kafmm_destroy(kafmm_plan plan) { free_plan(plan); }
+
+const char* kafmm_status_string(int s) {
+  switch (s) {
+    case KAFMM_OK: return "ok";
+    case KAFMM_EINVAL: return "invalid argument";
+    case KAFMM_EDOMAIN: return "point outside [0,1)^3";
+    case KAFMM_ENONFINITE: return "non-finite input";
+    case KAFMM_ENOMEM: return "out of memory";
+    case KAFMM_ECUDA: return "CUDA error";
+    case KAFMM_ENCCL: return "NCCL error";
+    case KAFMM_ESTATE: return "invalid state";
+    default: return "unknown status";
+  }
+}
+
+const char* kafmm_last_error(void) { return g_last_error.c_str(); }
+
+kafmm_status kafmm_get_info(kafmm_plan plan, kafmm_info* info) {
+  if (!plan || !info) return KAFMM_EINVAL;
+  Plan& P = *plan;
+  std::memset(info, 0, sizeof(*info));
+  info->n_points = P.n;
+  info->kernel = P.kernel;
+  info->p = P.p;
+  info->max_pts = P.cap;
+  info->depth = P.depth;
+  info->k_s = P.ks;
+  info->k_t = P.kt;
+  info->n_surf = P.M;
+  info->n_equiv = P.neq;
+  info->kept_up = P.kept_up;
+  info->kept_dn = P.kept_dn;
+  info->n_boxes = P.nbox;
+  info->n_leaves = P.nleaf;
+  info->n_u_pairs = P.n_u;
+  info->n_v_pairs = P.n_v;
+  info->n_w_pairs = P.n_w;
+  info->n_p2p = P.n_p2p;
+  info->workspace_bytes = P.bytes;
+  return KAFMM_OK;
+}
+
+kafmm_status kafmm_get_tree(kafmm_plan plan, int32_t* level, int32_t* ijk, int32_t* parent, int32_t* is_leaf,
+                            int64_t* pt_begin, int64_t* pt_end) {
+  if (!plan) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  Plan& P = *plan;
+  const int64_t nb = P.nbox;
+  if (level) KF_CUDA(cudaMemcpy(level, P.d_level, nb * 4, cudaMemcpyDeviceToHost));
+  if (ijk) KF_CUDA(cudaMemcpy(ijk, P.d_ijk, nb * 12, cudaMemcpyDeviceToHost));
+  if (parent) KF_CUDA(cudaMemcpy(parent, P.d_parent, nb * 4, cudaMemcpyDeviceToHost));
+  if (is_leaf) {
+    std::string tmp(nb, '\0');
+    KF_CUDA(cudaMemcpy(&tmp[0], P.d_leaf, nb, cudaMemcpyDeviceToHost));
+    for (int64_t b = 0; b < nb; ++b) is_leaf[b] = tmp[b] ? 1 : 0;
+  }
+  if (pt_begin) KF_CUDA(cudaMemcpy(pt_begin, P.d_pbeg, nb * 8, cudaMemcpyDeviceToHost));
+  if (pt_end) KF_CUDA(cudaMemcpy(pt_end, P.d_pend, nb * 8, cudaMemcpyDeviceToHost));
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_get_permutation(kafmm_plan plan, int64_t* perm) {
+  if (!plan || !perm) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  KF_CUDA(cudaMemcpy(perm, plan->d_perm, plan->n * 8, cudaMemcpyDeviceToHost));
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_get_list(kafmm_plan plan, int which, int32_t* tgt, int32_t* src) {
+  if (!plan || !tgt || !src) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  Plan& P = *plan;
+  std::vector<int32_t> leaves(P.nleaf);
+  KF_CUDA(cudaMemcpy(leaves.data(), P.d_leaf_ids, P.nleaf * 4, cudaMemcpyDeviceToHost));
+  if (which == 'U' || which == 'W') {
+    int64_t cnt = which == 'U' ? P.n_u : P.n_w;
+    std::vector<int64_t> off(P.nleaf + 1);
+    KF_CUDA(cudaMemcpy(off.data(), which == 'U' ? P.d_u_off : P.d_w_off, (P.nleaf + 1) * 8, cudaMemcpyDeviceToHost));
+    if (cnt) KF_CUDA(cudaMemcpy(src, which == 'U' ? P.d_u_src : P.d_w_src, cnt * 4, cudaMemcpyDeviceToHost));
+    for (int64_t s = 0; s < P.nleaf; ++s)
+      for (int64_t e = off[s]; e < off[s + 1]; ++e) tgt[e] = leaves[s];
+  } else if (which == 'V') {
+    std::vector<int2> pr(P.n_v);
+    if (P.n_v) KF_CUDA(cudaMemcpy(pr.data(), P.d_v_pairs, P.n_v * 8, cudaMemcpyDeviceToHost));
+    for (int64_t e = 0; e < P.n_v; ++e) {
+      tgt[e] = pr[e].y;
+      src[e] = pr[e].x;
+    }
+  } else if (which == 'X') {
+    std::vector<int32_t> tg(P.n_xbox);
+    std::vector<int64_t> off(P.n_xbox + 1);
+    if (P.n_xbox) {
+      KF_CUDA(cudaMemcpy(tg.data(), P.d_x_tgt, P.n_xbox * 4, cudaMemcpyDeviceToHost));
+      KF_CUDA(cudaMemcpy(off.data(), P.d_x_off, (P.n_xbox + 1) * 8, cudaMemcpyDeviceToHost));
+      KF_CUDA(cudaMemcpy(src, P.d_x_src, P.n_w * 4, cudaMemcpyDeviceToHost));
+    }
+    for (int64_t s = 0; s < P.n_xbox; ++s)
+      for (int64_t e = off[s]; e < off[s + 1]; ++e) tgt[e] = tg[s];
+  } else {
+    throw Error{KAFMM_EINVAL, "kafmm_get_list: which must be U, V, W or X"};
+  }
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_set_timing(kafmm_plan plan, int on) {
+  if (!plan) return KAFMM_EINVAL;
+  plan->timing = on != 0;
+  return KAFMM_OK;
+}
+
+kafmm_status kafmm_stage_times(kafmm_plan plan, float* ms) {
+  if (!plan || !ms) return KAFMM_EINVAL;
+  for (int s = 0; s < KAFMM_N_STAGES; ++s) ms[s] = plan->stage_ms[s];
+  return KAFMM_OK;
+}
+
+const char* kafmm_stage_name(int s) {
+  static const char* names[KAFMM_N_STAGES] = {"gather_src", "s2m",      "uc2ue", "m2m",     "m2l",        "s2l",
+                                              "dc2de+l2l",  "l2l(in dc2de)", "l2t+m2t", "p2p", "scatter_out", "total"};
+  return (s >= 0 && s < KAFMM_N_STAGES) ? names[s] : "?";
+}
+
+kafmm_status kafmm_launch_count(kafmm_plan plan, int* n) {
+  if (!plan || !n) return KAFMM_EINVAL;
+  *n = plan->launches;
+  return KAFMM_OK;
+}
+
+}  // extern "C"

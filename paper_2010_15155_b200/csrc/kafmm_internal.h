@@ -1,0 +1,176 @@
+// Internal plan structure shared by the translation units of libkafmm.so.
+// Not part of the ABI (include/kafmm.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/kafmm.h"
+
+namespace kafmm {
+
+// Morton keys: 21 bits per axis, x in the highest bit of each 3-bit group, so
+// the 3-bit group of a level is the child octant 4*cx + 2*cy + cz.
+constexpr int QBITS = 21;
+constexpr int MAX_LEVEL = 20;
+constexpr int N_OFFSETS = 316;  // {-3..3}^3 minus {-1..1}^3 (V-list offsets)
+
+// Surface radii in units of the box half-width (reading R1).
+constexpr double ALPHA_UE = 1.05, ALPHA_UC = 2.95, ALPHA_DC = 1.05, ALPHA_DE = 2.95;
+constexpr double TAU = 1e-12;  // SVD truncation (reading R2)
+
+// Tiling of the grouped FP64 GEMM (gemm_dmma.cuh).
+constexpr int GEMM_BM = 128, GEMM_BN = 64, GEMM_BK = 16;
+
+struct GemmTile {  // one CTA column-tile: up to GEMM_BN items sharing operator `op`
+  int op;
+  int item0;
+  int nitem;
+  int pad_;
+  double alpha;
+};
+
+enum GemmMode { GEMM_STORE = 0, GEMM_ADD = 1, GEMM_ATOMIC = 2 };
+
+struct GemmBatch {  // one launch of the grouped GEMM
+  std::vector<GemmTile> h_tiles;
+  GemmTile* d_tiles = nullptr;
+  int2* d_items = nullptr;  // x = input column (box / leaf slot), y = output column
+  int64_t n_items = 0;
+  int ntiles() const { return (int)h_tiles.size(); }
+};
+
+struct LevelRange {
+  int64_t begin, end;  // box ids [begin, end) of one level
+};
+
+enum Stage {
+  ST_GATHER = 0, ST_S2M, ST_UC2UE, ST_M2M, ST_M2L, ST_S2L, ST_DC2DE, ST_L2L,
+  ST_LEAF_FAR, ST_P2P, ST_SCATTER, ST_TOTAL
+};
+
+struct Plan {
+  // problem
+  int kernel = 0, p = 0, cap = 0;
+  int64_t n = 0;
+  int ks = 0, kt = 0;   // user source / target dims
+  int kml = 0;          // ML-tree kernel dimension: 1 (L) or 3 (G)
+  int srec = 0;         // doubles per sorted source record (4 Laplace, 8 Stokes family)
+  int M = 0, neq = 0, ldn = 0;   // surface points, equivalent vector length, padded
+  int kept_up = 0, kept_dn = 0, ldk = 0;
+  cudaStream_t stream = 0;
+  bool timing = false;
+  cudaEvent_t ev[ST_TOTAL + 1] = {};
+  float stage_ms[ST_TOTAL + 1] = {};
+  int launches = 0;
+
+  // tree (device unless noted)
+  int depth = 0;
+  int64_t nbox = 0, nleaf = 0;
+  std::vector<LevelRange> levels;  // host
+  int32_t* d_level = nullptr;
+  int32_t* d_ijk = nullptr;        // 3 per box
+  int32_t* d_parent = nullptr;
+  int32_t* d_child = nullptr;      // 8 per box, -1 if empty
+  uint8_t* d_leaf = nullptr;
+  int64_t* d_pbeg = nullptr;
+  int64_t* d_pend = nullptr;
+  uint64_t* d_key = nullptr;       // Morton prefix of the box at its level
+  int64_t* d_perm = nullptr;       // Morton position -> user index
+  double* d_pts = nullptr;         // sorted points, 4 doubles each (x, y, z, 0)
+
+  // lists (CSR, device)
+  int32_t* d_leaf_ids = nullptr;   // all leaves, level-major
+  int64_t* d_u_off = nullptr;      // per leaf slot
+  int32_t* d_u_src = nullptr;
+  int64_t* d_w_off = nullptr;      // per leaf slot
+  int32_t* d_w_src = nullptr;
+  int64_t n_u = 0, n_w = 0, n_v = 0, n_p2p = 0;
+  int32_t* d_s2m_ids = nullptr;    // leaves at level >= 2 (S2M jobs)
+  int64_t n_s2m = 0;
+  int32_t* d_x_tgt = nullptr;      // boxes with a non-empty X list
+  int64_t* d_x_off = nullptr;
+  int32_t* d_x_src = nullptr;
+  int64_t n_xbox = 0;
+  int2* d_v_pairs = nullptr;       // (src, tgt) sorted by (level, offset) -- also the M2L items
+
+  // operators (device, padded row-major)
+  double* d_surf = nullptr;        // M x 3 unit lattice offsets (-1 + 2 i/(p-1))
+  double* d_W1 = nullptr;          // UC2UE first factor  S^-1 U^T   (kept_up x ldn)
+  double* d_W2 = nullptr;          // UC2UE second factor V          (neq x ldk)
+  double* d_D1 = nullptr;          // DC2DE first factor             (kept_dn x ldn)
+  double* d_D2 = nullptr;          // DC2DE second factor            (neq x ldk)
+  double* d_m2m = nullptr;         // 8 x (neq_pad x ldn)
+  double* d_l2l = nullptr;         // 8 x (neq_pad x ldn)
+  double* d_m2l = nullptr;         // 316 x (neq_pad x ldn)
+  int64_t op_stride = 0;           // elements between consecutive n x n operators
+  int rows_pad = 0;                // neq rounded up to GEMM_BM
+  std::vector<double> h_sigma;
+
+  // GEMM batches
+  GemmBatch g_uc2ue_1, g_uc2ue_2;              // S2M leaves (level >= 2)
+  std::vector<GemmBatch> g_m2m;                // per parent level, bottom-up order
+  GemmBatch g_m2l;
+  std::vector<GemmBatch> g_dc2de_1, g_dc2de_2, g_l2l;  // per level (2..depth)
+
+  // workspaces (device)
+  double* d_rec = nullptr;         // n x srec sorted source records
+  double* d_outs = nullptr;        // n x kt sorted outputs
+  double* d_ue = nullptr;          // nbox x ldn
+  double* d_chk = nullptr;         // nbox x ldn (upward check at leaves, then downward check)
+  double* d_de = nullptr;          // nbox x ldn
+  double* d_t = nullptr;           // nbox x ldk (first-factor temporaries)
+  double* d_stage_in = nullptr;    // n x ks (eval_host staging)
+  double* d_stage_out = nullptr;   // n x kt
+  int* d_flag = nullptr;
+  int64_t bytes = 0;
+
+  std::vector<void*> allocs;
+};
+
+// error handling -----------------------------------------------------------
+void set_error(const std::string& msg);
+struct Error {
+  kafmm_status st;
+  std::string msg;
+};
+#define KF_CUDA(call)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      throw ::kafmm::Error{e_ == cudaErrorMemoryAllocation ? KAFMM_ENOMEM : KAFMM_ECUDA,     \
+                           std::string(#call) + ": " + cudaGetErrorString(e_)};              \
+  } while (0)
+#define KF_CHECK_LAUNCH() KF_CUDA(cudaGetLastError())
+
+template <class T>
+T* dalloc(Plan& P, size_t count) {
+  void* p = nullptr;
+  size_t b = count * sizeof(T);
+  if (b == 0) b = 8;
+  KF_CUDA(cudaMalloc(&p, b));
+  KF_CUDA(cudaMemsetAsync(p, 0, b, P.stream));
+  P.allocs.push_back(p);
+  P.bytes += (int64_t)b;
+  return (T*)p;
+}
+
+inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+// translation units
+void build_tree_and_lists(Plan& P, const double* d_points);   // kafmm_tree.cu
+void build_operators(Plan& P);                               // kafmm_ops.cu
+void build_gemm_batches(Plan& P);                            // kafmm_tree.cu
+void upload_batch(Plan& P, GemmBatch& g, const std::vector<int2>& h_items);
+void run_eval(Plan& P, const double* d_src, double* d_out);  // kafmm_eval.cu
+void check_values(Plan& P, const double* d_src);             // kafmm_eval.cu
+void launch_gemm(Plan& P, const GemmBatch& g, const double* A, int M, int K, int lda,
+                 const double* B, int ldb, double* C, int ldc, int mode);  // kafmm_gemm.cu
+
+}  // namespace kafmm
+
+// the opaque ABI handle is the plan itself
+struct kafmm_plan_s : public kafmm::Plan {};

@@ -1,0 +1,210 @@
+"""ctypes binding of libkafmm.so (include/kafmm.h).  Argument marshalling only.
+
+PyTorch is used for device memory and streams: tensors are passed to the C
+ABI as raw pointers (``Tensor.data_ptr()``).  Every step of the evaluation
+runs in the library's CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+KERNELS = {"laplace_pgrad": 1, "stokeslet": 2, "rpy": 3, "stokes_reg_vel": 4}
+N_STAGES = 12
+
+
+class KafmmError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: status {status} ({detail})")
+        self.status = status
+
+
+class Info(C.Structure):
+    _fields_ = [("n_points", C.c_int64), ("kernel", C.c_int), ("p", C.c_int), ("max_pts", C.c_int),
+                ("depth", C.c_int), ("k_s", C.c_int), ("k_t", C.c_int), ("n_surf", C.c_int),
+                ("n_equiv", C.c_int), ("kept_up", C.c_int), ("kept_dn", C.c_int),
+                ("n_boxes", C.c_int64), ("n_leaves", C.c_int64), ("n_u_pairs", C.c_int64),
+                ("n_v_pairs", C.c_int64), ("n_w_pairs", C.c_int64), ("n_p2p", C.c_int64),
+                ("workspace_bytes", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def lib_path() -> str:
+    return os.environ.get("KAFMM_LIB", os.path.join(HERE, "libkafmm.so"))
+
+
+_LIB = None
+
+# (name, restype, argtypes)
+_SIGS = [
+    ("kafmm_kernel_dims", C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("kafmm_setup", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("kafmm_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kafmm_eval", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("kafmm_eval_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("kafmm_check_values", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kafmm_sync", C.c_int, [C.c_void_p]),
+    ("kafmm_destroy", None, [C.c_void_p]),
+    ("kafmm_status_string", C.c_char_p, [C.c_int]),
+    ("kafmm_last_error", C.c_char_p, []),
+    ("kafmm_get_info", C.c_int, [C.c_void_p, C.POINTER(Info)]),
+    ("kafmm_get_tree", C.c_int, [C.c_void_p] + [C.c_void_p] * 6),
+    ("kafmm_get_permutation", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kafmm_get_list", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    ("kafmm_set_timing", C.c_int, [C.c_void_p, C.c_int]),
+    ("kafmm_stage_times", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("kafmm_stage_name", C.c_char_p, [C.c_int]),
+    ("kafmm_launch_count", C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+]
+EXPORTED = [s[0] for s in _SIGS]
+
+
+def load_library():
+    """Load libkafmm.so (raises if it is missing: there is no fallback)."""
+    global _LIB
+    if _LIB is None:
+        path = lib_path()
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (run python -m paper_2010_15155_b200.build)")
+        lib = C.CDLL(path)
+        for name, res, args in _SIGS:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        lib = load_library()
+        raise KafmmError(st, where, (lib.kafmm_last_error() or b"").decode())
+
+
+def kernel_dims(kernel) -> tuple[int, int]:
+    lib = load_library()
+    ks, kt = C.c_int(), C.c_int()
+    k = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+    _check(lib.kafmm_kernel_dims(k, C.byref(ks), C.byref(kt)), "kafmm_kernel_dims")
+    return ks.value, kt.value
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("kafmm: no CUDA device (there is no CPU fallback)")
+    return torch
+
+
+class KAFMM:
+    """A plan: octree, lists and operators for one point set (sources = targets).
+
+    points: (n, 3) float64 in [0,1)^3, numpy array or CUDA tensor.
+    """
+
+    def __init__(self, points, kernel: str, p: int, max_pts: int, stream=None):
+        torch = _torch()
+        self.lib = load_library()
+        self.kernel = kernel
+        if isinstance(points, np.ndarray):
+            pts = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float64)).cuda()
+        else:
+            pts = points.to(device="cuda", dtype=torch.float64).contiguous()
+        self.n = int(pts.shape[0])
+        self.k_s, self.k_t = kernel_dims(kernel)
+        h = C.c_void_p()
+        torch.cuda.synchronize()
+        _check(self.lib.kafmm_setup(C.c_void_p(pts.data_ptr()), self.n, KERNELS[kernel], int(p), int(max_pts),
+                                    C.byref(h)), "kafmm_setup")
+        self.h = h
+        if stream is not None:
+            self.set_stream(stream)
+
+    def set_stream(self, stream):
+        ptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        _check(self.lib.kafmm_set_stream(self.h, C.c_void_p(ptr)), "kafmm_set_stream")
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            self.lib.kafmm_destroy(h)
+            self.h = None
+
+    def close(self):
+        self.__del__()
+
+    # hot path
+    def eval(self, src, out=None):
+        """src: (n, k_s) float64 CUDA tensor (user order) -> (n, k_t) CUDA tensor."""
+        torch = _torch()
+        assert src.is_cuda and src.dtype == torch.float64 and src.shape == (self.n, self.k_s)
+        src = src.contiguous()
+        if out is None:
+            out = torch.empty((self.n, self.k_t), dtype=torch.float64, device=src.device)
+        _check(self.lib.kafmm_eval(self.h, C.c_void_p(src.data_ptr()), C.c_void_p(out.data_ptr())), "kafmm_eval")
+        return out
+
+    def eval_host(self, src: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """End-to-end through the C ABI with host buffers (copies inside)."""
+        assert src.dtype == np.float64 and src.shape == (self.n, self.k_s) and src.flags.c_contiguous
+        if out is None:
+            out = np.empty((self.n, self.k_t))
+        _check(self.lib.kafmm_eval_host(self.h, C.c_void_p(src.ctypes.data), C.c_void_p(out.ctypes.data)),
+               "kafmm_eval_host")
+        return out
+
+    def check_values(self, src):
+        _check(self.lib.kafmm_check_values(self.h, C.c_void_p(src.data_ptr())), "kafmm_check_values")
+
+    def sync(self):
+        _check(self.lib.kafmm_sync(self.h), "kafmm_sync")
+
+    # introspection
+    def info(self) -> Info:
+        inf = Info()
+        _check(self.lib.kafmm_get_info(self.h, C.byref(inf)), "kafmm_get_info")
+        return inf
+
+    def tree(self) -> dict:
+        nb = self.info().n_boxes
+        lev = np.empty(nb, np.int32)
+        ijk = np.empty((nb, 3), np.int32)
+        par = np.empty(nb, np.int32)
+        leaf = np.empty(nb, np.int32)
+        pb = np.empty(nb, np.int64)
+        pe = np.empty(nb, np.int64)
+        ptrs = [C.c_void_p(a.ctypes.data) for a in (lev, ijk, par, leaf, pb, pe)]
+        _check(self.lib.kafmm_get_tree(self.h, *ptrs), "kafmm_get_tree")
+        return dict(level=lev, ijk=ijk, parent=par, leaf=leaf.astype(bool), pbeg=pb, pend=pe)
+
+    def permutation(self) -> np.ndarray:
+        perm = np.empty(self.n, np.int64)
+        _check(self.lib.kafmm_get_permutation(self.h, C.c_void_p(perm.ctypes.data)), "kafmm_get_permutation")
+        return perm
+
+    def lists(self, which: str):
+        inf = self.info()
+        n = {"U": inf.n_u_pairs, "V": inf.n_v_pairs, "W": inf.n_w_pairs, "X": inf.n_w_pairs}[which]
+        tgt = np.empty(max(n, 1), np.int32)
+        src = np.empty(max(n, 1), np.int32)
+        _check(self.lib.kafmm_get_list(self.h, ord(which), C.c_void_p(tgt.ctypes.data), C.c_void_p(src.ctypes.data)),
+               "kafmm_get_list")
+        return tgt[:n], src[:n]
+
+    def set_timing(self, on: bool):
+        _check(self.lib.kafmm_set_timing(self.h, int(on)), "kafmm_set_timing")
+
+    def stage_times(self) -> dict:
+        arr = (C.c_float * N_STAGES)()
+        _check(self.lib.kafmm_stage_times(self.h, arr), "kafmm_stage_times")
+        return {self.lib.kafmm_stage_name(i).decode(): float(arr[i]) for i in range(N_STAGES)}
+
+    def launch_count(self) -> int:
+        n = C.c_int()
+        _check(self.lib.kafmm_launch_count(self.h, C.byref(n)), "kafmm_launch_count")
+        return n.value
