@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the KAFMM evaluation pass (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+Metric (BASELINE.json): FMM eval points/s = (N_S + N_T) / t_eval at fixed p.
+A step is one kafmm_eval (gather, S2M, UC2UE, M2M, M2L, S2L, DC2DE, L2L,
+L2T, M2T, P2P, scatter) over config C's synthetic cloud (default C2 =
+BASELINE configs[1], 1M points Laplace PGrad p=10 cap 64), inputs resident
+in HBM.  L2 is flushed (256 MiB write) before every timed step, outside the
+timed interval; each step is bracketed by CUDA events on the plan's stream.
+"e2e" times kafmm_eval_host: pinned host values -> device, eval, -> host.
+
+Multi-GPU (torchrun, N > 1): every rank evaluates its own instance of the
+workload (weak scaling, no data-path collective); the Morton-partitioned
+single-problem path is listed as NEXT in DESIGN.md.  Time = max over ranks.
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on a
+bounded sample of the same workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as WL  # noqa: E402
+
+# nominal flops per pair of the P2P kernels (rsqrt counted as 8)
+P2P_FLOPS = {"laplace_pgrad": 27, "stokeslet": 36, "rpy": 56, "stokes_reg_vel": 39}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="kafmm", choices=["kafmm", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
+    return ap.parse_args()
+
+
+def workload_name(spec):
+    return (f"C{spec.cid}: {spec.kernel}, N={spec.n}, {spec.cloud} cloud, p={spec.p}, "
+            f"max {spec.cap} pts/leaf, open BC, fp64")
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        try:
+            rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        except Exception:
+            rows = []
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+def _oracle_ops(spec):
+    """Oracle operators incl. all 316 M2L matrices: setup, not timed as eval."""
+    from oracle import fmm as F
+    from oracle.operators import v_offsets
+    op = F.operators(F.TABLES[spec.kernel]["ML"], spec.p)
+    for o in v_offsets():
+        op.m2l[o]
+    return op
+
+
+def _oracle_sample(spec, pts, vals, n_leaves_sample, seed, tree, op):
+    from oracle import fmm as F
+    smp = F.sample_leaves(tree, 1, seed=seed)
+    rng = np.random.default_rng(seed)
+    leaves = tree.leaves()
+    smp = sorted(int(b) for b in rng.choice(leaves, size=min(n_leaves_sample, leaves.size), replace=False))
+    tm = {}
+    F.fmm(pts, vals, spec.kernel, spec.p, spec.cap, target_leaves=smp, tree=tree, ops=op, timings=tm)
+    return smp, tm
+
+
+def oracle_sample_rate(spec, pts, vals, budget_s):
+    """Oracle throughput on a bounded sample of the workload (cpu_baseline).
+
+    One oracle call in sampled mode: the full upward pass (S2M, UC2UE, M2M
+    over every leaf and box) plus the downward pass and near field of a seeded
+    sample of whole leaves.  Full-eval time is extrapolated as
+    t_upward + t_downward * n_leaves / n_sample_leaves.  List building is
+    setup (like the GPU plan) and not counted.
+    """
+    from oracle import fmm as F
+    from oracle.tree import Tree
+    t = Tree(pts, spec.cap)
+    op = _oracle_ops(spec)
+    nl = t.leaves().size
+    smp, tm = _oracle_sample(spec, pts, vals, 16, 0, t, op)
+    n_trg = sum(t.pts[b].size for b in smp)
+    t_full = tm["upward"] + tm["downward"] * nl / len(smp)
+    cores = len(os.sched_getaffinity(0))
+    return dict(value=2 * spec.n / t_full, unit="points/s", cores=cores, kind="oracle",
+                sample=(f"oracle (numpy/scipy, {cores} host threads) on {spec.name}: full upward pass "
+                        f"{tm['upward']:.1f} s + downward pass and near field of {len(smp)} sampled leaves "
+                        f"({n_trg} targets) {tm['downward']:.2f} s, extrapolated to all {nl} leaves "
+                        f"= {t_full:.0f} s per eval"))
+
+
+def run_reference(args, spec, pts, vals, rank):
+    if rank != 0:
+        return
+    from oracle import fmm as F
+    from oracle.tree import Tree
+    t = Tree(pts, spec.cap)
+    op = _oracle_ops(spec)
+    nl = t.leaves().size
+    per, ups = [], []
+    s, warm, steps = 0, args.warmup, args.steps
+    while s < warm + steps:
+        # a step = the oracle's upward pass + downward/near field of 4 sampled leaves,
+        # prorated to the full evaluation
+        smp, tm = _oracle_sample(spec, pts, vals, 4, 1000 + s, t, op)
+        if s >= warm:
+            per.append(tm["upward"] + tm["downward"] * nl / len(smp))
+            ups.append(tm["upward"])
+        if s == 0 and tm["upward"] * (warm + steps) > 120:
+            # keep the arm within a few minutes: the first call (which also builds the
+            # lazily cached M2L matrices) counts as the only warm-up step
+            warm, steps = 1, max(1, min(steps, int(120 // max(tm["upward"], 1.0))))
+        s += 1
+    args.warmup = warm
+    ms = 1e3 * statistics.mean(per)
+    value = 2 * spec.n / (ms * 1e-3)
+    cores = len(os.sched_getaffinity(0))
+    line = {"impl": "reference", "metric": "FMM eval points/sec (N_S+N_T) at fixed p", "value": value,
+            "unit": "points/s", "n_gpus": args.gpus, "steps": len(per), "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(spec), "kernel": spec.kernel, "n": spec.n, "p": spec.p,
+                       "max_pts_per_leaf": spec.cap},
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
+                             "sample": (f"per step: oracle upward pass (mean {statistics.mean(ups):.1f} s) + "
+                                        f"downward pass and near field of 4 sampled leaves, extrapolated to "
+                                        f"{nl} leaves")},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    spec = WL.CONFIGS[args.config]
+    spec_pts = WL.make_points(spec)
+    vals = WL.make_values(spec, spec_pts.shape[0])
+
+    if args.impl == "reference":
+        run_reference(args, spec, spec_pts, vals, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_15155_b200 import KAFMM
+    from paper_2010_15155_b200.kafmm import fp64_peak
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    plan = KAFMM(spec_pts, spec.kernel, spec.p, spec.cap, stream=stream)
+    info = plan.info()
+    src = torch.from_numpy(vals).cuda()
+    out = torch.empty((spec.n, info.k_t), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        plan.eval(src, out)
+    barrier()
+
+    plan.set_timing(True)  # per-stage CUDA events on the plan's stream
+    step_ms, stages = [], []
+    with ClockSampler(local) as clk:
+        barrier()
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            plan.eval(src, out)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            stages.append(plan.stage_times())
+        barrier()
+    clocks = clk.summary()
+    plan.set_timing(False)
+    launches = plan.launch_count() * args.steps
+
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = float(tot.item()) / args.steps
+    value = world * 2 * spec.n / (ms * 1e-3)
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hsrc = torch.from_numpy(vals).pin_memory().numpy()
+        hout = torch.empty((spec.n, info.k_t), dtype=torch.float64).pin_memory().numpy()
+        plan.eval_host(hsrc, hout)
+        et = []
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            plan.eval_host(hsrc, hout)
+            et.append(time.perf_counter() - t0)
+        e = torch.tensor([sum(et)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e, op=dist.ReduceOp.MAX)
+        e_s = float(e.item()) / args.steps
+        e2e = {"value": world * 2 * spec.n / e_s, "unit": "points/s", "ms_per_step": 1e3 * e_s,
+               "h2d_bytes_per_step": int(vals.nbytes), "d2h_bytes_per_step": int(hout.nbytes)}
+
+    # roofline of the dominant kernel: M2L, dense FP64 contraction on DMMA
+    m2l_ms = statistics.mean(s["m2l"] for s in stages)
+    p2p_ms = statistics.mean(s["p2p"] for s in stages)
+    n = info.n_equiv
+    m2l_flop = 2.0 * n * n * info.n_v_pairs
+    peak_dmma = fp64_peak("dmma")
+    peak_dfma = fp64_peak("dfma")
+    achieved = m2l_flop / (m2l_ms * 1e-3) / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_C{spec.cid}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("m2l_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    p2p_flop = P2P_FLOPS[spec.kernel] * info.n_p2p
+    stage_mean = {k: round(statistics.mean(s[k] for s in stages), 4) for k in stages[0]}
+
+    line = {
+        "metric": "FMM eval points/sec (N_S+N_T) at fixed p", "value": value, "unit": "points/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": workload_name(spec), "kernel": spec.kernel, "n": spec.n, "p": spec.p,
+                   "max_pts_per_leaf": spec.cap, "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": f"{world} independent replicas" if world > 1 else "1 GPU"},
+        "roofline": {"kernel": "m2l (k_gemm_dmma, dense, grouped by V offset)", "bound": "tensor",
+                     "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s", "frac": achieved / peak_dmma,
+                     "traffic": traffic,
+                     "peak_source": "measured in this run: DMMA.8x8x4 loop (kafmm_fp64_peak); "
+                                    "MEASURED_PEAKS.json has no FP64 entry",
+                     "algorithmic": f"2 n^2 flop per V pair, n={n}, {info.n_v_pairs} pairs = {m2l_flop:.3e} flop"},
+        "p2p": {"achieved_tflops": p2p_flop / (p2p_ms * 1e-3) / 1e12, "peak_dfma": peak_dfma,
+                "frac": p2p_flop / (p2p_ms * 1e-3) / 1e12 / peak_dfma, "pairs": info.n_p2p,
+                "flop_per_pair": P2P_FLOPS[spec.kernel], "ms": p2p_ms},
+        "stages_ms": stage_mean,
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = {k: v for k, v in oracle_sample_rate(spec, spec_pts, vals, args.cpu_budget).items()
+                                if k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -152,6 +152,11 @@ const char* kafmm_stage_name(int stage);
 /* Kernel launches issued by one kafmm_eval. */
 kafmm_status kafmm_launch_count(kafmm_plan plan, int* n);
 
+/* FP64 throughput of the current device (roofline denominator; no FP64 figure
+ * is in MEASURED_PEAKS.json): which = 0 DMMA.8x8x4 tensor-core loop,
+ * 1 DFMA loop, over 4 CTAs of 256 threads per SM.  Result in TFLOP/s. */
+kafmm_status kafmm_fp64_peak(int which, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

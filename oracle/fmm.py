@@ -24,6 +24,8 @@ product per offset on stacked vectors; the arithmetic is unchanged.
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 
 from . import lists as L
@@ -71,14 +73,19 @@ def direct(kernel: str, points, values, trg_idx=None) -> np.ndarray:
 
 
 def fmm(points, values, kernel: str, p: int, cap: int, target_leaves=None,
-        tree: Tree | None = None, ops: Operators | None = None, keep_internals=False):
+        tree: Tree | None = None, ops: Operators | None = None, keep_internals=False,
+        timings: dict | None = None):
     """Evaluate the KAFMM sum.
 
     target_leaves=None: every target (returns out in user order, N x k_t).
     target_leaves=list: sampled mode -- full upward pass, downward pass only
     for the ancestors of those leaves; returns values at their points.
     Returns dict(out=..., idx=target point indices, tree=..., ops=...).
+    timings (optional dict) receives wall seconds of the list building
+    ('lists'), the upward pass ('upward') and the rest ('downward').
     """
+    clock = time.perf_counter
+    t_start = clock()
     tab = TABLES[kernel]
     points = np.asarray(points, dtype=np.float64)
     values = np.asarray(values, dtype=np.float64)
@@ -114,6 +121,7 @@ def fmm(points, values, kernel: str, p: int, cap: int, target_leaves=None,
     lstart = [int(ids[0]) for ids in level_boxes]
 
     # ---- upward pass: S->M at leaves, M->M bottom-up ---------------------------
+    t_lists = clock()
     ue_store = {}
     ue_next = None
     for l in range(t.depth, -1, -1):
@@ -143,6 +151,7 @@ def fmm(points, values, kernel: str, p: int, cap: int, target_leaves=None,
         ue_next = ue_l
 
     # ---- downward pass: M->L (V), S->L (X), DC2DE, L->L -------------------------
+    t_up = clock()
     de = {}
     for l in range(2, t.depth + 1):
         tb = sorted(b for b in tboxes if t.level[b] == l)
@@ -194,6 +203,9 @@ def fmm(points, values, kernel: str, p: int, cap: int, target_leaves=None,
         idx_all.append(idx)
     idx_all = np.concatenate(idx_all) if idx_all else np.zeros(0, dtype=np.int64)
     g_all = np.concatenate(out_rows) if out_rows else np.zeros((0, k_t))
+    if timings is not None:
+        t_end = clock()
+        timings.update(lists=t_lists - t_start, upward=t_up - t_lists, downward=t_end - t_up)
     res = dict(tree=t, ops=op, kept=(op.up_kept, op.dn_kept))
     if full:
         out = np.zeros((points.shape[0], k_t))

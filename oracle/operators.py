@@ -21,6 +21,7 @@ the composed M2M and L2L are level independent.
 """
 from __future__ import annotations
 
+import functools
 import itertools
 
 import numpy as np
@@ -36,13 +37,20 @@ H0 = 0.5
 C0 = np.array([0.5, 0.5, 0.5])
 
 
+@functools.lru_cache(maxsize=None)
+def _lattice(m: int) -> np.ndarray:
+    out = [(i, j, k) for i in range(m) for j in range(m) for k in range(m)
+           if min(i, j, k) == 0 or max(i, j, k) == m - 1]
+    a = np.array(out, dtype=np.float64)
+    a.setflags(write=False)
+    return a
+
+
 def surface_lattice(m: int) -> np.ndarray:
     """Integer lattice indices of the boundary of an m^3 cube, lexicographic."""
     if m < 2:
         raise ValueError("m >= 2")
-    out = [(i, j, k) for i in range(m) for j in range(m) for k in range(m)
-           if min(i, j, k) == 0 or max(i, j, k) == m - 1]
-    return np.array(out, dtype=np.float64)
+    return _lattice(m)
 
 
 def surface(m: int, c, h: float, alpha: float) -> np.ndarray:

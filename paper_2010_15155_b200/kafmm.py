@@ -60,6 +60,7 @@ _SIGS = [
     ("kafmm_stage_times", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     ("kafmm_stage_name", C.c_char_p, [C.c_int]),
     ("kafmm_launch_count", C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+    ("kafmm_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double)]),
 ]
 EXPORTED = [s[0] for s in _SIGS]
 
@@ -92,6 +93,14 @@ def kernel_dims(kernel) -> tuple[int, int]:
     k = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
     _check(lib.kafmm_kernel_dims(k, C.byref(ks), C.byref(kt)), "kafmm_kernel_dims")
     return ks.value, kt.value
+
+
+def fp64_peak(which: str = "dmma") -> float:
+    """Measured FP64 TFLOP/s of the device: 'dmma' (tensor core) or 'dfma'."""
+    lib = load_library()
+    v = C.c_double()
+    _check(lib.kafmm_fp64_peak(0 if which == "dmma" else 1, C.byref(v)), "kafmm_fp64_peak")
+    return v.value
 
 
 def _torch():
