@@ -1,0 +1,94 @@
+"""Edge cases of the CUDA path: degenerate trees, duplicates, boundaries,
+invalid input, and properties that hold at any size."""
+import numpy as np
+import pytest
+
+import workloads as WL
+from oracle import fmm as F
+from paper_2010_15155_b200 import KAFMM, KafmmError
+
+from .gpu_helpers import run_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kernel", WL.KERNELS)
+def test_single_point(kernel):
+    pts = np.array([[0.3, 0.2, 0.9]])
+    vals = WL.random_values(kernel, 1, 1)
+    _, out = run_gpu(pts, vals, kernel, 4, 8)
+    np.testing.assert_allclose(out, F.direct(kernel, pts, vals), rtol=1e-14, atol=1e-300)
+
+
+@pytest.mark.parametrize("kernel", WL.KERNELS)
+def test_single_leaf_equals_direct(kernel):
+    pts = np.random.default_rng(2).random((300, 3))
+    vals = WL.random_values(kernel, 300, 3)
+    plan, out = run_gpu(pts, vals, kernel, 6, 300)
+    assert plan.info().n_boxes == 1
+    d = F.direct(kernel, pts, vals)
+    assert F.rel_l2(out, d) < 1e-14
+
+
+@pytest.mark.parametrize("kernel", ["laplace_pgrad", "stokes_reg_vel"])
+def test_duplicate_points_and_zero_values(kernel):
+    rng = np.random.default_rng(4)
+    base = rng.random((700, 3))
+    pts = np.concatenate([base, base[:300]])   # exact duplicates: r^2 == 0 pairs across indices
+    vals = WL.random_values(kernel, 1000, 5)
+    plan, out = run_gpu(pts, vals, kernel, 6, 24)
+    ref = F.fmm(pts, vals, kernel, 6, 24)["out"]
+    assert max(F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) for lo, hi in F.blocks(kernel)) <= 1e-10
+    z = np.zeros_like(vals)
+    if z.shape[1] == 4:
+        z[:, 3] = vals[:, 3]
+    import torch
+    assert float(plan.eval(torch.from_numpy(z).cuda()).abs().max()) == 0.0
+
+
+def test_points_on_cell_boundaries_and_max_depth():
+    # coordinates on dyadic planes (a point on a plane goes to the upper box) and a
+    # tight cluster that forces the level-20 cap
+    g = (np.arange(8) / 8.0)
+    grid = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    tight = 0.5 + 1e-7 * np.random.default_rng(6).random((40, 3))
+    pts = np.concatenate([grid, tight])
+    vals = WL.random_values("stokeslet", pts.shape[0], 7)
+    plan, out = run_gpu(pts, vals, "stokeslet", 5, 4)
+    ref = F.fmm(pts, vals, "stokeslet", 5, 4)
+    assert plan.info().depth == ref["tree"].depth == 20
+    assert F.rel_l2(out, ref["out"]) <= 1e-10
+
+
+def test_invalid_inputs_fail_loudly():
+    pts = np.random.default_rng(8).random((100, 3))
+    bad = pts.copy()
+    bad[5, 1] = 1.0
+    with pytest.raises(KafmmError) as e:
+        KAFMM(bad, "stokeslet", 4, 10)
+    assert e.value.status == 2   # KAFMM_EDOMAIN
+    bad[5, 1] = np.nan
+    with pytest.raises(KafmmError) as e:
+        KAFMM(bad, "stokeslet", 4, 10)
+    assert e.value.status == 3   # KAFMM_ENONFINITE
+    import torch
+    plan = KAFMM(pts, "rpy", 4, 10)
+    v = torch.from_numpy(WL.random_values("rpy", 100, 9)).cuda()
+    plan.check_values(v)
+    v[3, 3] = -1.0
+    with pytest.raises(KafmmError):
+        plan.check_values(v)
+
+
+def test_superposition_and_scale_covariance_at_size():
+    # linearity in the forces and exact power-of-two covariance hold at any size
+    import torch
+    spec, pts, vals = WL.make_config(1, n=20000)
+    plan = KAFMM(pts, "stokeslet", 8, 50)
+    v1 = torch.from_numpy(vals).cuda()
+    v2 = torch.from_numpy(WL.random_values("stokeslet", 20000, 11)).cuda()
+    a, b, c = plan.eval(v1), plan.eval(v2), plan.eval(v1 + 3 * v2)
+    assert float((c - a - 3 * b).norm() / c.norm()) < 1e-11  # rounding x 1/sigma_min
+    half = KAFMM(pts * 0.5, "stokeslet", 8, 50)
+    h = half.eval(v1)
+    assert float((h - 2 * a).norm() / h.norm()) < 1e-11

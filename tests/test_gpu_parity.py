@@ -98,6 +98,7 @@ def test_error_vs_direct_within_2x_oracle(case):
 
 
 def test_eval_host_matches_eval(case):
-    # same path with host buffers; fp64 atomics reorder sums, so not bitwise
+    # same path with host buffers; fp64 atomics reorder sums (run-to-run ~1e-13
+    # after the 1/sigma_min amplification of the check->equivalent solve)
     out = case["plan"].eval_host(np.ascontiguousarray(case["vals"]))
-    assert F.rel_l2(out, case["gpu"]) < 1e-13
+    assert F.rel_l2(out, case["gpu"]) < 1e-11
