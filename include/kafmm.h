@@ -149,6 +149,16 @@ kafmm_status kafmm_get_list(kafmm_plan plan, int which, int32_t* tgt, int32_t* s
 kafmm_status kafmm_set_timing(kafmm_plan plan, int on);
 kafmm_status kafmm_stage_times(kafmm_plan plan, float* ms /* KAFMM_N_STAGES */);
 const char* kafmm_stage_name(int stage);
+/* M2L variant used by kafmm_eval:
+ *   0 = dense: raw kernel matrices grouped by V offset on the FP64 tensor cores
+ *   1 = FFT (default when p is in {4,5,6,7,8,10,12}): convolution on the (2p)^3
+ *       lattice grid, per-frequency products blocked by parent neighbourhoods.
+ * Both compute the same matrices; results agree to rounding.  EINVAL for an
+ * unknown mode or FFT with an unsupported p.  (Environment KAFMM_M2L=dense at
+ * setup selects dense.) */
+kafmm_status kafmm_set_m2l_mode(kafmm_plan plan, int mode);
+kafmm_status kafmm_get_m2l_mode(kafmm_plan plan, int* mode);
+
 /* Kernel launches issued by one kafmm_eval. */
 kafmm_status kafmm_launch_count(kafmm_plan plan, int* n);
 

@@ -1,6 +1,8 @@
 // extern "C" boundary of libkafmm.so (include/kafmm.h).  Every entry point
 // catches internal errors and turns them into a kafmm_status; the detail
 // string is kept per thread for kafmm_last_error().
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -90,6 +92,16 @@ kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int
   build_tree_and_lists(*P, points);
   build_operators(*P);
   build_gemm_batches(*P);
+  {
+    size_t fr = 0, tot = 0;
+    KF_CUDA(cudaMemGetInfo(&fr, &tot));
+    int64_t budget = std::min<int64_t>((int64_t)16 << 30, (int64_t)(fr / 4));
+    const char* env = getenv("KAFMM_FFT_BUDGET_MB");
+    if (env) budget = (int64_t)atoll(env) << 20;
+    build_fft_m2l(*P, budget);
+    const char* m = getenv("KAFMM_M2L");
+    if (m && std::string(m) == "dense") P->m2l_mode = M2L_DENSE;
+  }
   P->d_rec = dalloc<double>(*P, (size_t)n * P->srec);
   P->d_outs = dalloc<double>(*P, (size_t)n * kt);
   P->d_ue = dalloc<double>(*P, (size_t)P->nbox * P->ldn);
@@ -296,6 +308,22 @@ const char* kafmm_stage_name(int s) {
   static const char* names[KAFMM_N_STAGES] = {"gather_src", "s2m",      "uc2ue", "m2m",     "m2l",        "s2l",
                                               "dc2de+l2l",  "l2l(in dc2de)", "l2t+m2t", "p2p", "scatter_out", "total"};
   return (s >= 0 && s < KAFMM_N_STAGES) ? names[s] : "?";
+}
+
+kafmm_status kafmm_set_m2l_mode(kafmm_plan plan, int mode) {
+  if (!plan || (mode != 0 && mode != 1)) return KAFMM_EINVAL;
+  if (mode == 1 && plan->fft_chunks.empty() && plan->depth >= 2) {
+    set_error("FFT M2L not available for this p");
+    return KAFMM_EINVAL;
+  }
+  plan->m2l_mode = mode;
+  return KAFMM_OK;
+}
+
+kafmm_status kafmm_get_m2l_mode(kafmm_plan plan, int* mode) {
+  if (!plan || !mode) return KAFMM_EINVAL;
+  *mode = plan->m2l_mode;
+  return KAFMM_OK;
 }
 
 kafmm_status kafmm_launch_count(kafmm_plan plan, int* n) {

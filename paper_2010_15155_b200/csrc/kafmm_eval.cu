@@ -285,7 +285,10 @@ static void eval_impl(Plan& P, const double* d_src, double* d_out) {
   for (auto& g : P.g_m2m) launch_gemm(P, g, P.d_m2m, P.neq, P.ldn, P.ldn, P.d_ue, P.ldn, P.d_ue, P.ldn, GEMM_ATOMIC);
   KF_CUDA(cudaMemsetAsync(P.d_chk, 0, (size_t)P.nbox * P.ldn * 8, st));
   mark(ST_M2L);
-  launch_gemm(P, P.g_m2l, P.d_m2l, P.neq, P.ldn, P.ldn, P.d_ue, P.ldn, P.d_chk, P.ldn, GEMM_ATOMIC);
+  if (P.m2l_mode == M2L_FFT)
+    run_m2l_fft(P);
+  else
+    launch_gemm(P, P.g_m2l, P.d_m2l, P.neq, P.ldn, P.ldn, P.d_ue, P.ldn, P.d_chk, P.ldn, GEMM_ATOMIC);
   mark(ST_S2L);
   if (P.n_xbox > 0) {
     k_points_to_surface<KS, SREC, true><<<(unsigned)P.n_xbox, PT_THREADS, 0, st>>>(

@@ -47,6 +47,20 @@ struct LevelRange {
   int64_t begin, end;  // box ids [begin, end) of one level
 };
 
+// FFT M2L work unit: a Morton-contiguous range of target parents at level-1,
+// its target boxes (their children, a contiguous id range) and the source
+// boxes (children of the parents' colleagues), sized to a memory budget.
+struct FftChunk {
+  int level = 0;
+  int64_t npar = 0, ns = 0, nt = 0;
+  int64_t t0 = 0;            // first target box id; local target t = id - t0
+  int32_t* d_src = nullptr;  // ns source box ids (sorted)
+  int2* d_nbr = nullptr;     // npar x 26: (local index of the colleague's first child, child mask)
+  int2* d_par = nullptr;     // npar: (local index of the parent's first child, child mask)
+};
+
+enum M2LMode { M2L_DENSE = 0, M2L_FFT = 1 };
+
 enum Stage {
   ST_GATHER = 0, ST_S2M, ST_UC2UE, ST_M2M, ST_M2L, ST_S2L, ST_DC2DE, ST_L2L,
   ST_LEAF_FAR, ST_P2P, ST_SCATTER, ST_TOTAL
@@ -110,6 +124,17 @@ struct Plan {
   int rows_pad = 0;                // neq rounded up to GEMM_BM
   std::vector<double> h_sigma;
 
+  // FFT M2L (convolution on the (2p)^3 lattice grid)
+  int m2l_mode = M2L_FFT;
+  int NG = 0, NZ = 0, NF = 0;      // grid 2p, half-spectrum p+1, bins NG*NG*NZ
+  int ncomp = 0;                   // stored components per operator spectrum: 1 (L) or 6 (sym. G)
+  double2* d_that = nullptr;       // [NF][316][ncomp] operator spectra at level 0
+  int16_t* d_lat = nullptr;        // M x 3 integer lattice coordinates of the surface points
+  std::vector<FftChunk> fft_chunks;
+  double2* d_uhat = nullptr;       // [max_ns][kml][NF]
+  double2* d_chat = nullptr;       // [max_nt][kml][NF]
+  int64_t fft_max_ns = 0, fft_max_nt = 0;
+
   // GEMM batches
   GemmBatch g_uc2ue_1, g_uc2ue_2;              // S2M leaves (level >= 2)
   std::vector<GemmBatch> g_m2m;                // per parent level, bottom-up order
@@ -169,6 +194,8 @@ void run_eval(Plan& P, const double* d_src, double* d_out);  // kafmm_eval.cu
 void check_values(Plan& P, const double* d_src);             // kafmm_eval.cu
 void launch_gemm(Plan& P, const GemmBatch& g, const double* A, int M, int K, int lda,
                  const double* B, int ldb, double* C, int ldc, int mode);  // kafmm_gemm.cu
+void build_fft_m2l(Plan& P, int64_t budget_bytes);           // kafmm_fft.cu
+void run_m2l_fft(Plan& P);                                   // kafmm_fft.cu
 
 }  // namespace kafmm
 

@@ -61,6 +61,8 @@ _SIGS = [
     ("kafmm_stage_name", C.c_char_p, [C.c_int]),
     ("kafmm_launch_count", C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     ("kafmm_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    ("kafmm_set_m2l_mode", C.c_int, [C.c_void_p, C.c_int]),
+    ("kafmm_get_m2l_mode", C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
 ]
 EXPORTED = [s[0] for s in _SIGS]
 
@@ -212,6 +214,15 @@ class KAFMM:
         arr = (C.c_float * N_STAGES)()
         _check(self.lib.kafmm_stage_times(self.h, arr), "kafmm_stage_times")
         return {self.lib.kafmm_stage_name(i).decode(): float(arr[i]) for i in range(N_STAGES)}
+
+    def set_m2l(self, mode: str):
+        """'dense' (FP64 tensor-core GEMMs) or 'fft' (lattice convolution)."""
+        _check(self.lib.kafmm_set_m2l_mode(self.h, {"dense": 0, "fft": 1}[mode]), "kafmm_set_m2l_mode")
+
+    def m2l(self) -> str:
+        m = C.c_int()
+        _check(self.lib.kafmm_get_m2l_mode(self.h, C.byref(m)), "kafmm_get_m2l_mode")
+        return ["dense", "fft"][m.value]
 
     def launch_count(self) -> int:
         n = C.c_int()
