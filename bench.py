@@ -276,19 +276,38 @@ def main():
         e2e = {"value": world * 2 * spec.n / e_s, "unit": "points/s", "ms_per_step": 1e3 * e_s,
                "h2d_bytes_per_step": int(vals.nbytes), "d2h_bytes_per_step": int(hout.nbytes)}
 
-    # roofline of the dominant kernel: M2L, dense FP64 contraction on DMMA
+    # roofline of the dominant kernel: the M2L product on the FP64 tensor cores
+    # (DMMA.8x8x4): the frequency-space products of the FFT M2L, or the dense
+    # per-offset GEMMs.  Algorithmic work per V pair:
+    #   FFT:   8 kml^2 flop per frequency bin (kml x kml complex multiply-adds), NF bins
+    #   dense: 2 n^2 flop, n = kml M
+    mode = plan.m2l()
     m2l_ms = statistics.mean(s["m2l"] for s in stages)
+    prod_ms = statistics.mean(s["m2l_product"] for s in stages)
     p2p_ms = statistics.mean(s["p2p"] for s in stages)
     n = info.n_equiv
-    m2l_flop = 2.0 * n * n * info.n_v_pairs
+    kml = n // info.n_surf
+    ng = 2 * spec.p - 1
+    nf = ng * ng * (ng // 2 + 1)
+    if mode == "fft":
+        m2l_flop = 8.0 * kml * kml * nf * info.n_v_pairs
+        algo = (f"FFT M2L: 8 kml^2 flop per V pair per frequency bin, kml={kml}, NF={nf} (grid {ng}^3), "
+                f"{info.n_v_pairs} V pairs = {m2l_flop:.3e} flop")
+        kname = "m2l product (k_m2l_dmma: per-frequency complex GEMM over parent blocks, DMMA.8x8x4)"
+    else:
+        m2l_flop = 2.0 * n * n * info.n_v_pairs
+        algo = f"dense M2L: 2 n^2 flop per V pair, n={n}, {info.n_v_pairs} pairs = {m2l_flop:.3e} flop"
+        kname = "m2l product (k_gemm_dmma: dense, grouped by V offset, DMMA.8x8x4)"
     peak_dmma = fp64_peak("dmma")
     peak_dfma = fp64_peak("dfma")
-    achieved = m2l_flop / (m2l_ms * 1e-3) / 1e12
+    achieved = m2l_flop / (prod_ms * 1e-3) / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_C{spec.cid}.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("m2l_dram_bytes_per_launch")
+            tj = json.load(open(tf))
+            if tj.get("m2l_mode") == mode:
+                traffic = tj.get("m2l_dram_bytes_per_launch")
         except Exception:
             traffic = None
     p2p_flop = P2P_FLOPS[spec.kernel] * info.n_p2p
@@ -301,13 +320,14 @@ def main():
         "data": "synthetic",
         "config": {"workload": workload_name(spec), "kernel": spec.kernel, "n": spec.n, "p": spec.p,
                    "max_pts_per_leaf": spec.cap, "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": f"{world} independent replicas" if world > 1 else "1 GPU"},
-        "roofline": {"kernel": "m2l (k_gemm_dmma, dense, grouped by V offset)", "bound": "tensor",
-                     "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s", "frac": achieved / peak_dmma,
-                     "traffic": traffic,
+                   "parallelism": f"{world} independent replicas" if world > 1 else "1 GPU",
+                   "m2l": mode},
+        "roofline": {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": peak_dmma,
+                     "unit": "TFLOP/s", "frac": achieved / peak_dmma, "traffic": traffic,
                      "peak_source": "measured in this run: DMMA.8x8x4 loop (kafmm_fp64_peak); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
-                     "algorithmic": f"2 n^2 flop per V pair, n={n}, {info.n_v_pairs} pairs = {m2l_flop:.3e} flop"},
+                     "algorithmic": algo, "kernel_ms": prod_ms, "m2l_stage_ms": m2l_ms,
+                     "m2l_stage_tflops": m2l_flop / (m2l_ms * 1e-3) / 1e12},
         "p2p": {"achieved_tflops": p2p_flop / (p2p_ms * 1e-3) / 1e12, "peak_dfma": peak_dfma,
                 "frac": p2p_flop / (p2p_ms * 1e-3) / 1e12 / peak_dfma, "pairs": info.n_p2p,
                 "flop_per_pair": P2P_FLOPS[spec.kernel], "ms": p2p_ms},

@@ -37,7 +37,7 @@ typedef struct kafmm_plan_s* kafmm_plan; /* opaque; owned by the library */
 
 typedef enum {
   KAFMM_OK = 0,
-  KAFMM_EINVAL = 1,     /* null pointer, n < 1, p < 2, max_pts < 1, unknown kernel */
+  KAFMM_EINVAL = 1,     /* null pointer, n < 1, n > 2^31-1, p < 2, max_pts < 1, unknown kernel */
   KAFMM_EDOMAIN = 2,    /* a point outside [0,1)^3 */
   KAFMM_ENONFINITE = 3, /* NaN/Inf in points or values, or negative b / eps */
   KAFMM_ENOMEM = 4,     /* device allocation failed */
@@ -144,8 +144,11 @@ kafmm_status kafmm_get_permutation(kafmm_plan plan, int64_t* perm);
 kafmm_status kafmm_get_list(kafmm_plan plan, int which, int32_t* tgt, int32_t* src);
 
 /* Per-stage device times (ms) of the most recent kafmm_eval when stage
- * timing is on (kafmm_set_timing(plan, 1)); names via kafmm_stage_name. */
-#define KAFMM_N_STAGES 12
+ * timing is on (kafmm_set_timing(plan, 1)); names via kafmm_stage_name.
+ * Slot 12 ("m2l_product") is the device time of the M2L product kernels
+ * alone (the frequency-space DMMA products of the FFT variant, or the dense
+ * DMMA GEMMs), a part of slot 4 ("m2l"). */
+#define KAFMM_N_STAGES 13
 kafmm_status kafmm_set_timing(kafmm_plan plan, int on);
 kafmm_status kafmm_stage_times(kafmm_plan plan, float* ms /* KAFMM_N_STAGES */);
 const char* kafmm_stage_name(int stage);
@@ -166,6 +169,37 @@ kafmm_status kafmm_launch_count(kafmm_plan plan, int* n);
  * is in MEASURED_PEAKS.json): which = 0 DMMA.8x8x4 tensor-core loop,
  * 1 DFMA loop, over 4 CTAs of 256 threads per SM.  Result in TFLOP/s. */
 kafmm_status kafmm_fp64_peak(int which, double* tflops);
+
+/* ---- multi-GPU building blocks (paper_2010_15155_b200/dist.py) ----
+ * One process per GPU.  Every rank builds the plan of the GLOBAL point set
+ * with kafmm_setup and then restricts it to a contiguous range of the
+ * Morton-sorted points (whole leaves), [plo, phi) in the order of
+ * kafmm_get_permutation.  The restricted plan's evaluation is split in two
+ * so the caller can exchange multipoles between the passes:
+ *   kafmm_eval_up    a1-a4 over the owned leaves (S2M, UC2UE) and M2M into
+ *                    every box whose subtree holds owned points; boxes that
+ *                    straddle ranks hold this rank's partial sum
+ *   (caller)         all-reduce the straddling boxes' UE, receive the ghost
+ *                    UE of remote boxes this rank's V/W lists name
+ *   kafmm_eval_down  a5-a12 for the active boxes and owned leaves; writes the
+ *                    rows of trg_out (user order) of the owned points only
+ * src_values of kafmm_eval_up is a full n x k_s user-order array of which the
+ * rows of owned points and of the remote U/X-list leaves must be valid.
+ * EINVAL if [plo, phi) is outside [0, n) or cuts a leaf; ESTATE if already
+ * restricted.  kafmm_eval on a restricted plan runs both passes back to back. */
+kafmm_status kafmm_restrict(kafmm_plan plan, int64_t plo, int64_t phi);
+kafmm_status kafmm_eval_up(kafmm_plan plan, const double* src_values);
+kafmm_status kafmm_eval_down(kafmm_plan plan, double* trg_out);
+/* UE rows of boxes ids[0..n) (device int32) <-> buf (device, n x n_equiv,
+ * row-major), on the plan's stream. */
+kafmm_status kafmm_pack_ue(kafmm_plan plan, const int32_t* ids, int64_t n, double* buf);
+kafmm_status kafmm_unpack_ue(kafmm_plan plan, const int32_t* ids, int64_t n, const double* buf);
+/* Row movers on the plan's stream (device pointers, rows of ld doubles):
+ * gather dst[j] = src[idx[j]], scatter dst[idx[j]] = src[j], j < n. */
+kafmm_status kafmm_gather_rows(kafmm_plan plan, const double* src, int ld, const int64_t* idx, int64_t n,
+                               double* dst);
+kafmm_status kafmm_scatter_rows(kafmm_plan plan, const double* src, int ld, const int64_t* idx, int64_t n,
+                                double* dst);
 
 #ifdef __cplusplus
 }

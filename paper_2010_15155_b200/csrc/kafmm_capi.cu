@@ -29,6 +29,8 @@ static void free_plan(kafmm_plan_s* P) {
   for (void* p : P->allocs) cudaFree(p);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : P->prod_ev)
+    if (e) cudaEventDestroy(e);
   delete P;
 }
 }  // namespace kafmm
@@ -68,7 +70,7 @@ kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int
                          kafmm_plan* out) {
   if (out) *out = nullptr;
   int ks, kt;
-  if (!points || !out || n < 1 || p < 2 || max_pts_per_leaf < 1 || dims(kernel, &ks, &kt) != 0) {
+  if (!points || !out || n < 1 || n > INT32_MAX || p < 2 || max_pts_per_leaf < 1 || dims(kernel, &ks, &kt) != 0) {
     set_error("kafmm_setup: invalid argument");
     return KAFMM_EINVAL;
   }
@@ -143,6 +145,13 @@ kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_o
     KF_CUDA(cudaEventSynchronize(plan->ev[ST_TOTAL]));
     for (int s = 0; s < ST_TOTAL; ++s) KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[s], plan->ev[s], plan->ev[s + 1]));
     KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[ST_TOTAL], plan->ev[0], plan->ev[ST_TOTAL]));
+    float prod = 0.0f;
+    for (int i = 0; i + 1 < plan->prod_used; i += 2) {
+      float t = 0.0f;
+      KF_CUDA(cudaEventElapsedTime(&t, plan->prod_ev[i], plan->prod_ev[i + 1]));
+      prod += t;
+    }
+    plan->stage_ms[ST_M2L_PRODUCT] = prod;
   }
   return KAFMM_OK;
   KF_API_END
@@ -306,7 +315,8 @@ kafmm_status kafmm_stage_times(kafmm_plan plan, float* ms) {
 
 const char* kafmm_stage_name(int s) {
   static const char* names[KAFMM_N_STAGES] = {"gather_src", "s2m",      "uc2ue", "m2m",     "m2l",        "s2l",
-                                              "dc2de+l2l",  "l2l(in dc2de)", "l2t+m2t", "p2p", "scatter_out", "total"};
+                                              "dc2de+l2l",  "l2l(in dc2de)", "l2t+m2t", "p2p", "scatter_out", "total",
+                                              "m2l_product"};
   return (s >= 0 && s < KAFMM_N_STAGES) ? names[s] : "?";
 }
 
@@ -324,6 +334,70 @@ kafmm_status kafmm_get_m2l_mode(kafmm_plan plan, int* mode) {
   if (!plan || !mode) return KAFMM_EINVAL;
   *mode = plan->m2l_mode;
   return KAFMM_OK;
+}
+
+kafmm_status kafmm_restrict(kafmm_plan plan, int64_t plo, int64_t phi) {
+  if (!plan) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  restrict_plan(*plan, plo, phi);
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_eval_up(kafmm_plan plan, const double* src_values) {
+  if (!plan || !src_values) {
+    set_error("kafmm_eval_up: null argument");
+    return KAFMM_EINVAL;
+  }
+  KF_API_BEGIN
+  run_eval_up(*plan, src_values);
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_eval_down(kafmm_plan plan, double* trg_out) {
+  if (!plan || !trg_out) {
+    set_error("kafmm_eval_down: null argument");
+    return KAFMM_EINVAL;
+  }
+  KF_API_BEGIN
+  run_eval_down(*plan, trg_out);
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_pack_ue(kafmm_plan plan, const int32_t* ids, int64_t n, double* buf) {
+  if (!plan || n < 0 || (n > 0 && (!ids || !buf))) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  pack_ue(*plan, ids, n, buf);
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_unpack_ue(kafmm_plan plan, const int32_t* ids, int64_t n, const double* buf) {
+  if (!plan || n < 0 || (n > 0 && (!ids || !buf))) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  unpack_ue(*plan, ids, n, buf);
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_gather_rows(kafmm_plan plan, const double* src, int ld, const int64_t* idx, int64_t n,
+                               double* dst) {
+  if (!plan || ld < 1 || n < 0 || (n > 0 && (!src || !idx || !dst))) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  gather_rows(*plan, src, ld, idx, n, dst);
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_scatter_rows(kafmm_plan plan, const double* src, int ld, const int64_t* idx, int64_t n,
+                                double* dst) {
+  if (!plan || ld < 1 || n < 0 || (n > 0 && (!src || !idx || !dst))) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  scatter_rows(*plan, src, ld, idx, n, dst);
+  return KAFMM_OK;
+  KF_API_END
 }
 
 kafmm_status kafmm_launch_count(kafmm_plan plan, int* n) {

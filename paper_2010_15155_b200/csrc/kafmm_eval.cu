@@ -21,7 +21,6 @@
 namespace kafmm {
 
 constexpr int PT_THREADS = 128;  // pointwise kernels
-constexpr int SURF_TQ = 6;       // check points per thread per pass (768 >= M at p = 12)
 
 __device__ __forceinline__ void box_geom(const int32_t* __restrict__ level, const int32_t* __restrict__ ijk, int b,
                                          double& cx, double& cy, double& cz, double& h) {
@@ -55,60 +54,92 @@ __global__ void k_gather(const double* __restrict__ vals, const double* __restri
   }
 }
 
+// Source streaming shared by the pointwise kernels: the CTA walks a list of
+// point ranges (or generated surface points), copies them into one shared
+// chunk of CH records and runs the pair loop once per full chunk, so a
+// __syncthreads pair is paid per CH sources instead of per source leaf.
+constexpr int STREAM_DOUBLES = 2048;  // 16 KB of shared memory per CTA
+
+// copy `take` records of SREC doubles from rec[a ..] to chunk slot `fill`
+template <int SREC>
+__device__ __forceinline__ void copy_records(double* __restrict__ ss, int fill, const double* __restrict__ rec,
+                                             int64_t a, int take) {
+  const double2* g = reinterpret_cast<const double2*>(rec + a * SREC);
+  double2* s = reinterpret_cast<double2*>(ss + fill * SREC);
+  for (int idx = threadIdx.x; idx < take * (SREC / 2); idx += blockDim.x) s[idx] = g[idx];
+}
+
 // a2 / a6: points -> check surface of a box ------------------------------------
-// jobs[j] = target box; sources = the box's own points (src_off == nullptr, S2M)
-// or the leaves src_leaf[src_off[j] .. src_off[j+1]) (S2L over the X list).
-template <class K, int SREC, bool ADD>
+// jobs[j] = target box; sources = the box's own points (roff == nullptr, S2M)
+// or the merged point ranges rng[roff[j] .. roff[j+1]) of its X list (S2L).
+// TQ check points per thread (TQ * PT_THREADS >= M).
+template <class K, int SREC, int TQ, bool ADD>
 __global__ void __launch_bounds__(PT_THREADS)
-    k_points_to_surface(const int32_t* __restrict__ jobs, const int64_t* __restrict__ src_off,
-                        const int32_t* __restrict__ src_leaf, const int32_t* __restrict__ level,
+    k_points_to_surface(const int32_t* __restrict__ jobs, const int64_t* __restrict__ roff,
+                        const int2* __restrict__ rng, const int32_t* __restrict__ level,
                         const int32_t* __restrict__ ijk, const int64_t* __restrict__ pbeg,
                         const int64_t* __restrict__ pend, const double* __restrict__ rec,
                         const double* __restrict__ surf, int M, double alpha, double* __restrict__ out, int ldn) {
-  __shared__ __align__(16) double ss[PT_THREADS * SREC];
+  constexpr int CH = STREAM_DOUBLES / SREC;
+  __shared__ __align__(16) double ss[CH * SREC];
   const int job = blockIdx.x, tid = threadIdx.x;
   const int b = jobs[job];
   double cx, cy, cz, h;
   box_geom(level, ijk, b, cx, cy, cz, h);
   const double sc = alpha * h;
-  const int64_t e0 = src_off ? src_off[job] : 0, e1 = src_off ? src_off[job + 1] : 1;
-  for (int tb = 0; tb < M; tb += PT_THREADS * SURF_TQ) {
-    double tx[SURF_TQ], ty[SURF_TQ], tz[SURF_TQ], acc[SURF_TQ][K::KT];
+  double tx[TQ], ty[TQ], tz[TQ], acc[TQ][K::KT];
 #pragma unroll
-    for (int q = 0; q < SURF_TQ; ++q) {
-      int i = min(tb + tid + PT_THREADS * q, M - 1);
-      tx[q] = cx + sc * surf[3 * i];
-      ty[q] = cy + sc * surf[3 * i + 1];
-      tz[q] = cz + sc * surf[3 * i + 2];
+  for (int q = 0; q < TQ; ++q) {
+    int i = min(tid + PT_THREADS * q, M - 1);
+    tx[q] = cx + sc * surf[3 * i];
+    ty[q] = cy + sc * surf[3 * i + 1];
+    tz[q] = cz + sc * surf[3 * i + 2];
 #pragma unroll
-      for (int a = 0; a < K::KT; ++a) acc[q][a] = 0.0;
+    for (int a = 0; a < K::KT; ++a) acc[q][a] = 0.0;
+  }
+  auto run = [&](int cnt) {
+    __syncthreads();
+    for (int j = 0; j < cnt; ++j) {
+      const double* sr = ss + j * SREC;
+      const double sx = sr[0], sy = sr[1], sz = sr[2];
+#pragma unroll
+      for (int q = 0; q < TQ; ++q) K::acc(tx[q] - sx, ty[q] - sy, tz[q] - sz, sr + 3, acc[q]);
     }
-    for (int64_t e = e0; e < e1; ++e) {
-      const int leaf = src_off ? src_leaf[e] : b;
-      const int64_t p0 = pbeg[leaf], p1 = pend[leaf];
-      for (int64_t s0 = p0; s0 < p1; s0 += PT_THREADS) {
-        const int cnt = (int)((p1 - s0) < PT_THREADS ? (p1 - s0) : PT_THREADS);
-        __syncthreads();
-        for (int idx = tid; idx < cnt * SREC; idx += PT_THREADS) ss[idx] = rec[s0 * SREC + idx];
-        __syncthreads();
-        for (int j = 0; j < cnt; ++j) {
-          const double* sr = ss + j * SREC;
-          const double sx = sr[0], sy = sr[1], sz = sr[2];
-#pragma unroll
-          for (int q = 0; q < SURF_TQ; ++q) K::acc(tx[q] - sx, ty[q] - sy, tz[q] - sz, sr + 3, acc[q]);
-        }
+    __syncthreads();
+  };
+  const int64_t r0 = roff ? roff[job] : 0, r1 = roff ? roff[job + 1] : 1;
+  int fill = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    int64_t a, e;
+    if (roff) {
+      const int2 g = rng[r];
+      a = g.x;
+      e = g.y;
+    } else {
+      a = pbeg[b];
+      e = pend[b];
+    }
+    while (a < e) {
+      const int take = (int)min((int64_t)(CH - fill), e - a);
+      copy_records<SREC>(ss, fill, rec, a, take);
+      fill += take;
+      a += take;
+      if (fill == CH) {
+        run(CH);
+        fill = 0;
       }
     }
-    double* o = out + (int64_t)b * ldn;
+  }
+  if (fill) run(fill);
+  double* o = out + (int64_t)b * ldn;
 #pragma unroll
-    for (int q = 0; q < SURF_TQ; ++q) {
-      int i = tb + tid + PT_THREADS * q;
-      if (i < M) {
+  for (int q = 0; q < TQ; ++q) {
+    int i = tid + PT_THREADS * q;
+    if (i < M) {
 #pragma unroll
-        for (int a = 0; a < K::KT; ++a) {
-          if (ADD) o[i * K::KT + a] += acc[q][a];
-          else o[i * K::KT + a] = acc[q][a];
-        }
+      for (int a = 0; a < K::KT; ++a) {
+        if (ADD) o[i * K::KT + a] += acc[q][a];
+        else o[i * K::KT + a] = acc[q][a];
       }
     }
   }
@@ -145,6 +176,8 @@ __device__ __forceinline__ void slice_reduce_store(const Slice& z, double (&acc)
 }
 
 // a9 + a10: L2T (own downward equivalent, level >= 2) and M2T (W list) ------
+// Sources are generated surface points (lattice offset x radius + centre) with
+// their equivalent densities; SSTR doubles per source in the chunk.
 template <class K, int SSTR>
 __global__ void __launch_bounds__(PT_THREADS)
     k_leaf_far(const int32_t* __restrict__ leaves, const int32_t* __restrict__ level, const int32_t* __restrict__ ijk,
@@ -152,7 +185,8 @@ __global__ void __launch_bounds__(PT_THREADS)
                const int64_t* __restrict__ w_off, const int32_t* __restrict__ w_src, const double* __restrict__ ue,
                const double* __restrict__ de, int ldn, const double* __restrict__ surf, int M,
                double* __restrict__ outs) {
-  __shared__ __align__(16) double ss[PT_THREADS * SSTR];
+  constexpr int CH = STREAM_DOUBLES / SSTR;
+  __shared__ __align__(16) double ss[CH * SSTR];
   __shared__ double red[PT_THREADS * K::KT];
   const int job = blockIdx.x, tid = threadIdx.x;
   const int b = leaves[job];
@@ -167,49 +201,60 @@ __global__ void __launch_bounds__(PT_THREADS)
     double acc[K::KT];
 #pragma unroll
     for (int a = 0; a < K::KT; ++a) acc[a] = 0.0;
+    auto run = [&](int cnt) {
+      __syncthreads();
+      if (act)
+        for (int j = z.sl; j < cnt; j += z.S) {
+          const double* sr = ss + j * SSTR;
+          K::acc(tx - sr[0], ty - sr[1], tz - sr[2], sr + 3, acc);
+        }
+      __syncthreads();
+    };
+    int fill = 0;
     for (int64_t e = (lb >= 2 ? e0 - 1 : e0); e < e1; ++e) {
       const bool own = e < e0;
       const int sb = own ? b : w_src[e];
       const double* dens = (own ? de : ue) + (int64_t)sb * ldn;
       double cx, cy, cz, h;
       box_geom(level, ijk, sb, cx, cy, cz, h);
-      const double sc = (own ? 2.95 : 1.05) * h;  // ALPHA_DE / ALPHA_UE
-      for (int s0 = 0; s0 < M; s0 += PT_THREADS) {
-        const int cnt = min(PT_THREADS, M - s0);
-        __syncthreads();
-        if (tid < cnt) {
-          const int i = s0 + tid;
-          double* d = ss + tid * SSTR;
+      const double sc = (own ? ALPHA_DE : ALPHA_UE) * h;
+      for (int i0 = 0; i0 < M;) {
+        const int take = min(CH - fill, M - i0);
+        for (int idx = tid; idx < take; idx += PT_THREADS) {
+          const int i = i0 + idx;
+          double* d = ss + (fill + idx) * SSTR;
           d[0] = cx + sc * surf[3 * i];
           d[1] = cy + sc * surf[3 * i + 1];
           d[2] = cz + sc * surf[3 * i + 2];
 #pragma unroll
           for (int a = 0; a < K::KS; ++a) d[3 + a] = dens[i * K::KS + a];
         }
-        __syncthreads();
-        if (act)
-          for (int j = z.sl; j < cnt; j += z.S) {
-            const double* sr = ss + j * SSTR;
-            K::acc(tx - sr[0], ty - sr[1], tz - sr[2], sr + 3, acc);
-          }
+        fill += take;
+        i0 += take;
+        if (fill == CH) {
+          run(CH);
+          fill = 0;
+        }
       }
     }
+    if (fill) run(fill);
     slice_reduce_store<K::KT>(z, acc, red, outs + t0 * K::KT, false);
   }
 }
 
-// a11: P2P over the U list ----------------------------------------------------
+// a11: P2P over the U list: merged source ranges streamed through shared memory
 template <class K, int SREC>
 __global__ void __launch_bounds__(PT_THREADS)
     k_p2p(const int32_t* __restrict__ leaves, const int64_t* __restrict__ pbeg, const int64_t* __restrict__ pend,
-          const double* __restrict__ rec, const int64_t* __restrict__ u_off, const int32_t* __restrict__ u_src,
+          const double* __restrict__ rec, const int64_t* __restrict__ roff, const int2* __restrict__ rng,
           double* __restrict__ outs) {
-  __shared__ __align__(16) double ss[PT_THREADS * SREC];
+  constexpr int CH = STREAM_DOUBLES / SREC;
+  __shared__ __align__(16) double ss[CH * SREC];
   __shared__ double red[PT_THREADS * K::KT];
-  const int job = blockIdx.x, tid = threadIdx.x;
+  const int job = blockIdx.x;
   const int b = leaves[job];
   const int64_t p0 = pbeg[b], p1 = pend[b];
-  const int64_t e0 = u_off[job], e1 = u_off[job + 1];
+  const int64_t r0 = roff[job], r1 = roff[job + 1];
   for (int64_t t0 = p0; t0 < p1; t0 += PT_THREADS) {
     Slice z((int)((p1 - t0) < PT_THREADS ? (p1 - t0) : PT_THREADS));
     const bool act = z.sl < z.S;
@@ -218,21 +263,32 @@ __global__ void __launch_bounds__(PT_THREADS)
     double acc[K::KT];
 #pragma unroll
     for (int a = 0; a < K::KT; ++a) acc[a] = 0.0;
-    for (int64_t e = e0; e < e1; ++e) {
-      const int sb = u_src[e];
-      const int64_t q0 = pbeg[sb], q1 = pend[sb];
-      for (int64_t s0 = q0; s0 < q1; s0 += PT_THREADS) {
-        const int cnt = (int)((q1 - s0) < PT_THREADS ? (q1 - s0) : PT_THREADS);
-        __syncthreads();
-        for (int idx = tid; idx < cnt * SREC; idx += PT_THREADS) ss[idx] = rec[s0 * SREC + idx];
-        __syncthreads();
-        if (act)
-          for (int j = z.sl; j < cnt; j += z.S) {
-            const double* sr = ss + j * SREC;
-            K::acc(tx - sr[0], ty - sr[1], tz - sr[2], sr + 3, acc);
-          }
+    auto run = [&](int cnt) {
+      __syncthreads();
+      if (act)
+        for (int j = z.sl; j < cnt; j += z.S) {
+          const double* sr = ss + j * SREC;
+          K::acc(tx - sr[0], ty - sr[1], tz - sr[2], sr + 3, acc);
+        }
+      __syncthreads();
+    };
+    int fill = 0;
+    for (int64_t r = r0; r < r1; ++r) {
+      const int2 g = rng[r];
+      int64_t a = g.x;
+      const int64_t e = g.y;
+      while (a < e) {
+        const int take = (int)min((int64_t)(CH - fill), e - a);
+        copy_records<SREC>(ss, fill, rec, a, take);
+        fill += take;
+        a += take;
+        if (fill == CH) {
+          run(CH);
+          fill = 0;
+        }
       }
     }
+    if (fill) run(fill);
     slice_reduce_store<K::KT>(z, acc, red, outs + t0 * K::KT, true);
   }
 }
@@ -258,12 +314,34 @@ __global__ void k_check_values(const double* __restrict__ v, int64_t n, int ks, 
 // ---------------------------------------------------------------------------
 static inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
-template <class KS, class KT_, class KST, int SREC>
-static void eval_impl(Plan& P, const double* d_src, double* d_out) {
+// S2M / S2L launch with TQ = ceil(M / PT_THREADS) check points per thread
+template <class K, int SREC, bool ADD>
+static void launch_surface(Plan& P, const int32_t* jobs, int64_t njobs, const int64_t* roff, const int2* rng,
+                           double alpha) {
+  const int tq = (P.M + PT_THREADS - 1) / PT_THREADS;
+#define KF_SURF(TQ)                                                                                          \
+  k_points_to_surface<K, SREC, TQ, ADD><<<(unsigned)njobs, PT_THREADS, 0, P.stream>>>(                     \
+      jobs, roff, rng, P.d_level, P.d_ijk, P.d_pbeg, P.d_pend, P.d_rec, P.d_surf, P.M, alpha, P.d_chk, P.ldn)
+  if (tq <= 1) KF_SURF(1);
+  else if (tq == 2) KF_SURF(2);
+  else if (tq == 3) KF_SURF(3);
+  else if (tq == 4) KF_SURF(4);
+  else if (tq <= 6) KF_SURF(6);
+  else if (tq <= 8) KF_SURF(8);
+  else throw Error{KAFMM_EINVAL, "p too large for the surface kernels (M > 1024)"};
+#undef KF_SURF
+  KF_CHECK_LAUNCH();
+  P.launches++;
+}
+
+// a1-a4: gather, S2M, UC2UE, M2M (upward pass)
+template <class KS, int SREC>
+static void eval_up_impl(Plan& P, const double* d_src) {
   cudaStream_t st = P.stream;
   auto mark = [&](int s) {
     if (P.timing) KF_CUDA(cudaEventRecord(P.ev[s], st));
   };
+  const Jobs& J = P.J;
   P.launches = 0;
   mark(ST_GATHER);
   k_gather<<<nblk(P.n), 256, 0, st>>>(d_src, P.d_pts, P.d_perm, P.n, P.ks, SREC, P.d_rec);
@@ -271,69 +349,92 @@ static void eval_impl(Plan& P, const double* d_src, double* d_out) {
   P.launches++;
   KF_CUDA(cudaMemsetAsync(P.d_ue, 0, (size_t)P.nbox * P.ldn * 8, st));
   mark(ST_S2M);
-  if (P.n_s2m > 0) {
-    k_points_to_surface<KS, SREC, false><<<(unsigned)P.n_s2m, PT_THREADS, 0, st>>>(
-        P.d_s2m_ids, nullptr, nullptr, P.d_level, P.d_ijk, P.d_pbeg, P.d_pend, P.d_rec, P.d_surf, P.M, ALPHA_UC,
-        P.d_chk, P.ldn);
-    KF_CHECK_LAUNCH();
-    P.launches++;
-  }
+  if (J.ns2m > 0) launch_surface<KS, SREC, false>(P, J.s2m_ids, J.ns2m, nullptr, nullptr, ALPHA_UC);
   mark(ST_UC2UE);
   launch_gemm(P, P.g_uc2ue_1, P.d_W1, P.kept_up, P.ldn, P.ldn, P.d_chk, P.ldn, P.d_t, P.ldk, GEMM_STORE);
   launch_gemm(P, P.g_uc2ue_2, P.d_W2, P.neq, P.ldk, P.ldk, P.d_t, P.ldk, P.d_ue, P.ldn, GEMM_STORE);
   mark(ST_M2M);
   for (auto& g : P.g_m2m) launch_gemm(P, g, P.d_m2m, P.neq, P.ldn, P.ldn, P.d_ue, P.ldn, P.d_ue, P.ldn, GEMM_ATOMIC);
+}
+
+// a5-a12: M2L, S2L, DC2DE + L2L, L2T + M2T, P2P, scatter (downward pass and leaves)
+template <class KS, class KT_, class KST, int SREC>
+static void eval_down_impl(Plan& P, double* d_out) {
+  cudaStream_t st = P.stream;
+  auto mark = [&](int s) {
+    if (P.timing) KF_CUDA(cudaEventRecord(P.ev[s], st));
+  };
+  const Jobs& J = P.J;
   KF_CUDA(cudaMemsetAsync(P.d_chk, 0, (size_t)P.nbox * P.ldn * 8, st));
   mark(ST_M2L);
-  if (P.m2l_mode == M2L_FFT)
+  P.prod_used = 0;
+  if (P.m2l_mode == M2L_FFT) {
     run_m2l_fft(P);
-  else
+  } else {
+    prod_mark(P);
     launch_gemm(P, P.g_m2l, P.d_m2l, P.neq, P.ldn, P.ldn, P.d_ue, P.ldn, P.d_chk, P.ldn, GEMM_ATOMIC);
-  mark(ST_S2L);
-  if (P.n_xbox > 0) {
-    k_points_to_surface<KS, SREC, true><<<(unsigned)P.n_xbox, PT_THREADS, 0, st>>>(
-        P.d_x_tgt, P.d_x_off, P.d_x_src, P.d_level, P.d_ijk, P.d_pbeg, P.d_pend, P.d_rec, P.d_surf, P.M, ALPHA_DC,
-        P.d_chk, P.ldn);
-    KF_CHECK_LAUNCH();
-    P.launches++;
+    prod_mark(P);
   }
+  mark(ST_S2L);
+  if (J.nx > 0) launch_surface<KS, SREC, true>(P, J.x_tgt, J.nx, J.x_roff, J.x_rng, ALPHA_DC);
   mark(ST_DC2DE);
-  float l2l_ms = 0.0f;
   for (int l = 2; l <= P.depth; ++l) {
     int i = l - 2;
     launch_gemm(P, P.g_dc2de_1[i], P.d_D1, P.kept_dn, P.ldn, P.ldn, P.d_chk, P.ldn, P.d_t, P.ldk, GEMM_STORE);
     launch_gemm(P, P.g_dc2de_2[i], P.d_D2, P.neq, P.ldk, P.ldk, P.d_t, P.ldk, P.d_de, P.ldn, GEMM_STORE);
     if (l >= 3) launch_gemm(P, P.g_l2l[i], P.d_l2l, P.neq, P.ldn, P.ldn, P.d_de, P.ldn, P.d_de, P.ldn, GEMM_ADD);
   }
-  (void)l2l_ms;
   mark(ST_L2L);  // L2L is interleaved with DC2DE per level; its own slot stays empty
   mark(ST_LEAF_FAR);
-  k_leaf_far<KT_, 8><<<(unsigned)P.nleaf, PT_THREADS, 0, st>>>(P.d_leaf_ids, P.d_level, P.d_ijk, P.d_pbeg,
-                                                                P.d_pend, P.d_pts, P.d_w_off, P.d_w_src, P.d_ue,
-                                                                P.d_de, P.ldn, P.d_surf, P.M, P.d_outs);
-  KF_CHECK_LAUNCH();
-  P.launches++;
+  if (J.nleaf > 0) {
+    k_leaf_far<KT_, (3 + KT_::KS + 1) / 2 * 2><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(
+        J.leaf_ids, P.d_level, P.d_ijk, P.d_pbeg, P.d_pend, P.d_pts, J.w_off, J.w_src, P.d_ue, P.d_de, P.ldn,
+        P.d_surf, P.M, P.d_outs);
+    KF_CHECK_LAUNCH();
+    P.launches++;
+  }
   mark(ST_P2P);
-  k_p2p<KST, SREC><<<(unsigned)P.nleaf, PT_THREADS, 0, st>>>(P.d_leaf_ids, P.d_pbeg, P.d_pend, P.d_rec, P.d_u_off,
-                                                             P.d_u_src, P.d_outs);
-  KF_CHECK_LAUNCH();
-  P.launches++;
+  if (J.nleaf > 0) {
+    k_p2p<KST, SREC><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(J.leaf_ids, P.d_pbeg, P.d_pend, P.d_rec, J.u_roff,
+                                                               J.u_rng, P.d_outs);
+    KF_CHECK_LAUNCH();
+    P.launches++;
+  }
   mark(ST_SCATTER);
   const double scale = (P.kernel == KAFMM_LAPLACE_PGRAD) ? 1.0 / (4.0 * M_PI) : 1.0 / (8.0 * M_PI);
-  k_scatter<<<nblk(P.n * P.kt), 256, 0, st>>>(P.d_outs, P.d_perm, P.n, P.kt, scale, d_out);
-  KF_CHECK_LAUNCH();
-  P.launches++;
+  const int64_t cnt = (J.phi - J.plo) * P.kt;
+  if (cnt > 0) {
+    k_scatter<<<nblk(cnt), 256, 0, st>>>(P.d_outs + J.plo * P.kt, P.d_perm + J.plo, J.phi - J.plo, P.kt, scale,
+                                         d_out);
+    KF_CHECK_LAUNCH();
+    P.launches++;
+  }
   mark(ST_TOTAL);
 }
 
-void run_eval(Plan& P, const double* d_src, double* d_out) {
+void run_eval_up(Plan& P, const double* d_src) {
   switch (P.kernel) {
-    case KAFMM_LAPLACE_PGRAD: eval_impl<KL, KLG, KLG, 4>(P, d_src, d_out); break;
-    case KAFMM_STOKESLET: eval_impl<KG, KG, KG, 8>(P, d_src, d_out); break;
-    case KAFMM_RPY: eval_impl<KRPY, KGL, KRPYL, 8>(P, d_src, d_out); break;
-    case KAFMM_STOKES_REG_VEL: eval_impl<KGE, KG, KGE, 8>(P, d_src, d_out); break;
+    case KAFMM_LAPLACE_PGRAD: eval_up_impl<KL, 4>(P, d_src); break;
+    case KAFMM_STOKESLET: eval_up_impl<KG, 8>(P, d_src); break;
+    case KAFMM_RPY: eval_up_impl<KRPY, 8>(P, d_src); break;
+    case KAFMM_STOKES_REG_VEL: eval_up_impl<KGE, 8>(P, d_src); break;
     default: throw Error{KAFMM_EINVAL, "unknown kernel"};
   }
+}
+
+void run_eval_down(Plan& P, double* d_out) {
+  switch (P.kernel) {
+    case KAFMM_LAPLACE_PGRAD: eval_down_impl<KL, KLG, KLG, 4>(P, d_out); break;
+    case KAFMM_STOKESLET: eval_down_impl<KG, KG, KG, 8>(P, d_out); break;
+    case KAFMM_RPY: eval_down_impl<KRPY, KGL, KRPYL, 8>(P, d_out); break;
+    case KAFMM_STOKES_REG_VEL: eval_down_impl<KGE, KG, KGE, 8>(P, d_out); break;
+    default: throw Error{KAFMM_EINVAL, "unknown kernel"};
+  }
+}
+
+void run_eval(Plan& P, const double* d_src, double* d_out) {
+  run_eval_up(P, d_src);
+  run_eval_down(P, d_out);
 }
 
 void check_values(Plan& P, const double* d_src) {

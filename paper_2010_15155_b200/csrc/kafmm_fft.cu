@@ -1,4 +1,4 @@
-// M2L as a convolution on the regular (2p)^3 lattice grid (SURVEY.md §8(a) a5,
+// M2L as a convolution on the regular lattice grid (SURVEY.md §8(a) a5,
 // option b; the paper's M2L cost remark P:633 refers to PVFMM's FFT M2L).
 //
 // The upward-equivalent surface of a source box C and the downward-check
@@ -6,18 +6,19 @@
 // lattices with the same spacing delta = 2*1.05 h/(p-1).  For C = B + 2h o,
 //     check_B(I) = sum_J K(delta (I - J) - 2 h o) ue_C(J),   I, J in [0,p)^3,
 // a 3D linear convolution with the kernel grid t_o(D) = K(delta D - 2 h o),
-// D in [-(p-1), p-1]^3.  Zero-padded to NG = 2p it is a circular convolution:
+// D in [-(p-1), p-1]^3.  Zero-padded to NG = 2p - 1 (the smallest size at
+// which D -> D mod NG is one-to-one) it is a circular convolution:
 //     check_B = IDFT( sum_{C in V(B)} That_o . DFT(ue_C) )  on the lattice.
 // This is exactly the dense M2L (up to rounding): same matrices, factored.
 //
 // Hot path per level and chunk (all on the plan's stream):
-//   k_fft_fwd   one CTA per source box: real DFT of ue (p^3 cube, surface only
-//               non-zero) -> Uhat[box][comp][NG*NG*(p+1)], staged z, y, x in SMEM
-//   k_m2l_had   PVFMM-style blocking: for a frequency f and a target parent P,
-//               Chat[children of P](f) = sum over the 26 colleague directions d
-//               and the 8x8 (target child, source child) pairs of That_o(f)
-//               Uhat(f), o = 2d + oct(c) - oct(b), skipping adjacent pairs;
-//               CTA = 16 frequencies x NPB parents, accumulators in registers
+//   k_fft_fwd   one CTA per (source parent, child octant): real DFT of ue (p^3
+//               cube, surface only non-zero), staged z, y, x in shared memory,
+//               -> ub[f][parent][8 kml] (frequency-major, zero for a missing child)
+//   k_m2l_dmma  per frequency a complex GEMM over target parents: the 26
+//               colleague directions x 8x8 (target child, source child) blocks,
+//               o = 2d + oct(c) - oct(b), adjacent pairs zero (PVFMM-style
+//               blocking), on the FP64 tensor cores (DMMA.8x8x4)
 //   k_fft_inv   one CTA per target box: inverse DFT, evaluated only at the
 //               downward-check surface points, times 2^l / NG^3, added to CHK
 // Operator spectra That_o (316 offsets, level 0) are computed once at setup
@@ -33,14 +34,15 @@
 
 namespace kafmm {
 
-__constant__ int16_t c_fft_off_id[343];  // (ox+3)*49+(oy+3)*7+(oz+3) -> offset id (or -1)
-
 static inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
 // ---------------------------------------------------------------------------
 // setup: kernel grids t_o and their spectra
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int dmap(int g, int p, int NG) { return g < p ? g : (g > p ? g - NG : INT_MIN); }
+// grid index -> lattice difference D in [-(p-1), p-1] (NG >= 2p - 1), or INT_MIN for padding
+__device__ __forceinline__ int dmap(int g, int p, int NG) {
+  return g < p ? g : (g >= NG - (p - 1) ? g - NG : INT_MIN);
+}
 
 __global__ void k_kernel_grid(int p, int NG, int kml, double delta, const int8_t* __restrict__ offs, double* grid) {
   const int NG3 = NG * NG * NG;
@@ -85,24 +87,27 @@ __global__ void k_spectra_transpose(int NF, int nc, const double2* __restrict__ 
 // ---------------------------------------------------------------------------
 template <int P>
 struct FftDims {
-  static constexpr int NG = 2 * P, NZ = P + 1, NF = NG * NG * NZ;
+  static constexpr int NG = 2 * P - 1, NZ = NG / 2 + 1, NF = NG * NG * NZ;
   static constexpr int CUBE = (P * P * P + 1) / 2 * 2;  // doubles, keep 16-B alignment after it
   static constexpr size_t FWD_SMEM = (CUBE + 2 * (P * P * NZ + P * NG * NZ + NG)) * sizeof(double);
-  static constexpr size_t INV_SMEM = 2 * (P * NG * NZ + P * P * NZ + NG) * sizeof(double);
+  // spectrum column (later reused for the y-pass output) + x-pass output + twiddles
+  static constexpr size_t INV_SMEM = 2 * (NF + P * NG * NZ + NG) * sizeof(double);
 };
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
 __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
   acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
   acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
 }
 
+// forward: one CTA per (source parent q, child octant c); the child's upward
+// equivalent density on the p^3 lattice (non-zero on the surface only) ->
+// its real DFT on the NG^3 grid, staged z (real -> half spectrum), y, x in
+// shared memory, written to ub[f][q][c kml + e].  A missing child writes zeros.
 template <int P>
 __global__ void __launch_bounds__(256)
-    k_fft_fwd(const int32_t* __restrict__ src, const double* __restrict__ ue, int ldn, int kml,
-              const int16_t* __restrict__ lat, int M, double2* __restrict__ uhat) {
+    k_fft_fwd(const int32_t* __restrict__ qbox, const int32_t* __restrict__ child, int64_t nq,
+              const double* __restrict__ ue, int ldn, int kml, const int16_t* __restrict__ lat, int M,
+              double2* __restrict__ ub) {
   using D = FftDims<P>;
   constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF;
   extern __shared__ __align__(16) double sm[];
@@ -110,8 +115,15 @@ __global__ void __launch_bounds__(256)
   double2* A = reinterpret_cast<double2*>(sm + D::CUBE);  // [x][y][fz]
   double2* B = A + P * P * NZ;                              // [x][fy][fz]
   double2* tw = B + P * NG * NZ;                            // w^j = exp(-2 pi i j / NG)
-  const int s = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
-  const int64_t box = src[s];
+  const int64_t q = blockIdx.x >> 3;
+  const int c = blockIdx.x & 7, tid = threadIdx.x, bd = blockDim.x;
+  const int R = 8 * kml;
+  const int64_t box = child[8 * (int64_t)qbox[q] + c];
+  if (box < 0) {
+    for (int e = 0; e < kml; ++e)
+      for (int f = tid; f < NF; f += bd) ub[((int64_t)f * nq + q) * R + c * kml + e] = make_double2(0.0, 0.0);
+    return;
+  }
   for (int j = tid; j < NG; j += bd) {
     double sn, cs;
     sincospi(2.0 * j / NG, &sn, &cs);
@@ -125,13 +137,13 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     for (int idx = tid; idx < P * P * NZ; idx += bd) {  // z: real -> half spectrum
       int xy = idx / NZ, fz = idx - xy * NZ;
-      const double* c = cube + xy * P;
+      const double* cc = cube + xy * P;
       double re = 0.0, im = 0.0;
       int k = 0;
 #pragma unroll
       for (int z = 0; z < P; ++z) {
-        re = fma(c[z], tw[k].x, re);
-        im = fma(c[z], tw[k].y, im);
+        re = fma(cc[z], tw[k].x, re);
+        im = fma(cc[z], tw[k].y, im);
         k += fz;
         if (k >= NG) k -= NG;
       }
@@ -152,52 +164,59 @@ __global__ void __launch_bounds__(256)
       B[idx] = acc;
     }
     __syncthreads();
-    double2* out = uhat + ((int64_t)s * kml + e) * NF;
     for (int idx = tid; idx < NF; idx += bd) {  // x
       int fx = idx / (NG * NZ), r = idx - fx * NG * NZ;
-      const double2* b = B + r;
+      const double2* bb = B + r;
       double2 acc = make_double2(0.0, 0.0);
       int k = 0;
 #pragma unroll
       for (int x = 0; x < P; ++x) {
-        cmac(acc, b[x * NG * NZ], tw[k]);
+        cmac(acc, bb[x * NG * NZ], tw[k]);
         k += fx;
         if (k >= NG) k -= NG;
       }
-      out[idx] = acc;
+      ub[((int64_t)idx * nq + q) * R + c * kml + e] = acc;
     }
     __syncthreads();
   }
 }
 
+// inverse: one CTA per target box; its check spectrum cb[f][parent][b kml + a]
+// -> inverse DFT evaluated only at the downward-check surface points, times
+// 2^l / NG^3, added to CHK.  NG is odd, so there is no Nyquist bin.
 template <int P>
 __global__ void __launch_bounds__(256)
-    k_fft_inv(int64_t t0, const int32_t* __restrict__ level, const double2* __restrict__ chat, int kml,
+    k_fft_inv(const int32_t* __restrict__ tbox, const int2* __restrict__ tpb, int64_t npar,
+              const int32_t* __restrict__ level, const double2* __restrict__ cb, int kml,
               const int16_t* __restrict__ lat, int M, double* __restrict__ chk, int ldn) {
   using D = FftDims<P>;
   constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF;
   extern __shared__ __align__(16) double sm[];
-  double2* Dx = reinterpret_cast<double2*>(sm);  // [x][fy][fz]
-  double2* E = Dx + P * NG * NZ;                  // [x][y][fz]
-  double2* tw = E + P * P * NZ;                   // exp(+2 pi i j / NG)
+  double2* S = reinterpret_cast<double2*>(sm);  // [fx][fy][fz], then E [x][y][fz]
+  double2* Dx = S + NF;                          // [x][fy][fz]
+  double2* tw = Dx + P * NG * NZ;                // exp(+2 pi i j / NG)
+  double2* E = S;
   const int t = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
-  const int64_t box = t0 + t;
+  const int64_t box = tbox[t];
+  const int2 pb = tpb[t];
+  const int R = 8 * kml;
   const double scale = ldexp(1.0, level[box]) / (double)(NG * NG * NG);
   for (int j = tid; j < NG; j += bd) {
     double sn, cs;
     sincospi(2.0 * j / NG, &sn, &cs);
     tw[j] = make_double2(cs, sn);
   }
-  __syncthreads();
   for (int a = 0; a < kml; ++a) {
-    const double2* c = chat + ((int64_t)t * kml + a) * NF;
+    const double2* col = cb + (int64_t)pb.x * R + pb.y * kml + a;
+    for (int f = tid; f < NF; f += bd) S[f] = col[(int64_t)f * npar * R];
+    __syncthreads();
     for (int idx = tid; idx < P * NG * NZ; idx += bd) {  // x: only x in [0, P)
       int x = idx / (NG * NZ), r = idx - x * NG * NZ;
       double2 acc = make_double2(0.0, 0.0);
       int k = 0;
 #pragma unroll 4
       for (int fx = 0; fx < NG; ++fx) {
-        cmac(acc, c[fx * NG * NZ + r], tw[k]);
+        cmac(acc, S[fx * NG * NZ + r], tw[k]);
         k += x;
         if (k >= NG) k -= NG;
       }
@@ -222,96 +241,106 @@ __global__ void __launch_bounds__(256)
     for (int m = tid; m < M; m += bd) {  // z: half spectrum -> real, only at surface points
       int x = lat[3 * m], y = lat[3 * m + 1], z = lat[3 * m + 2];
       const double2* e = E + (x * P + y) * NZ;
-      double v = e[0].x;
+      double v = 0.0;
       int k = z;
-      for (int fz = 1; fz < P; ++fz) {
-        v += 2.0 * (e[fz].x * tw[k].x - e[fz].y * tw[k].y);
+      for (int fz = 1; fz < NZ; ++fz) {
+        v = fma(e[fz].x, tw[k].x, fma(-e[fz].y, tw[k].y, v));
         k += z;
         if (k >= NG) k -= NG;
       }
-      v += e[P].x * ((z & 1) ? -1.0 : 1.0);  // Nyquist bin
-      o[m * kml + a] += scale * v;
+      o[m * kml + a] += scale * fma(2.0, v, e[0].x);
     }
     __syncthreads();
   }
 }
 
-constexpr int HAD_THREADS = 128;
-constexpr int HAD_FPB = HAD_THREADS / 8;  // frequencies per block (8 target children per frequency)
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 
-template <int KML, int NPB>
-__global__ void __launch_bounds__(HAD_THREADS)
-    k_m2l_had(int NF, int npar, const double2* __restrict__ that, const double2* __restrict__ uhat,
-              double2* __restrict__ chat, const int2* __restrict__ par, const int2* __restrict__ nbr) {
-  constexpr int NC = KML == 1 ? 1 : 6;
-  __shared__ int2 s_nbr[NPB * 26];
-  __shared__ int2 s_par[NPB];
-  const int nbp = (npar + NPB - 1) / NPB;
-  const int pb = blockIdx.x % nbp, fc = blockIdx.x / nbp;
-  const int b = threadIdx.x & 7, fi = threadIdx.x >> 3;
-  const int f = fc * HAD_FPB + fi;
-  const bool fok = f < NF;
-  const int fs = fok ? f : NF - 1;
-  const int P0 = pb * NPB;
-  for (int i = threadIdx.x; i < NPB * 26; i += HAD_THREADS) {
-    int pp = P0 + i / 26;
-    s_nbr[i] = pp < npar ? nbr[(int64_t)P0 * 26 + i] : make_int2(0, 0);
-  }
-  for (int i = threadIdx.x; i < NPB; i += HAD_THREADS) s_par[i] = (P0 + i < npar) ? par[P0 + i] : make_int2(0, 0);
+// Hadamard stage on the FP64 tensor cores.  For one frequency f and a target
+// parent P, with Q_d the colleague of P in direction d (26 of them):
+//     C_P(f)[b, a] = sum_d sum_{c, e} T_{o(d,c,b)}(f)[a, e] U_{Q_d}(f)[c, e],
+//     o(d, c, b) = 2 d + oct(c) - oct(b),  T = 0 for adjacent (c, b)
+// i.e. per frequency a complex GEMM  C[8k x npar] = A_f[8k x 26*8k] B_f
+// whose A is the same for every parent.  A warp owns all 8k rows and NT x 8
+// parents; the A fragments are gathered from the frequency's operator spectra
+// in shared memory through a precomputed index table, the B fragments are the
+// colleagues' child blocks (one 16-B load per lane), and a complex product is
+// four DMMA.8x8x4 (re re, -im im, re im, im re).
+constexpr int DM_WARPS = 4;
+
+template <int KML, int NT>
+__global__ void __launch_bounds__(DM_WARPS * 32)
+    k_m2l_dmma(int64_t npar, int64_t nq, int npb, const double2* __restrict__ that, const double2* __restrict__ ub,
+               double2* __restrict__ cb, const int32_t* __restrict__ nbr, const int16_t* __restrict__ aidx) {
+  constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML, KS = R / 4, PPW = NT * 8;
+  __shared__ double2 sT[N_OFFSETS * NC];
+  const int64_t f = blockIdx.x / npb;
+  const int pb = blockIdx.x % npb;
+  for (int i = threadIdx.x; i < N_OFFSETS * NC; i += DM_WARPS * 32) sT[i] = that[f * N_OFFSETS * NC + i];
   __syncthreads();
-  double2 acc[NPB][KML];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int64_t P0 = ((int64_t)pb * DM_WARPS + warp) * PPW;
+  if (P0 >= npar) return;
+  double acc[KML][NT][2][2];
 #pragma unroll
-  for (int q = 0; q < NPB; ++q)
+  for (int m = 0; m < KML; ++m)
 #pragma unroll
-    for (int a = 0; a < KML; ++a) acc[q][a] = make_double2(0.0, 0.0);
-  const int bx = (b >> 2) & 1, by = (b >> 1) & 1, bz = b & 1;
-  const double2* tf = that + (int64_t)fs * N_OFFSETS * NC;
-  for (int dd = 0; dd < 26; ++dd) {
-    const int d = dd < 13 ? dd : dd + 1;  // skip the centre (0,0,0)
-    const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
-    for (int c = 0; c < 8; ++c) {
-      const int ox = 2 * dx + ((c >> 2) & 1) - bx, oy = 2 * dy + ((c >> 1) & 1) - by, oz = 2 * dz + (c & 1) - bz;
-      if (max(abs(ox), max(abs(oy), abs(oz))) < 2) continue;  // adjacent: U list, not V
-      const int oid = c_fft_off_id[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)];
-      double2 T[NC];
+    for (int n = 0; n < NT; ++n) acc[m][n][0][0] = acc[m][n][0][1] = acc[m][n][1][0] = acc[m][n][1][1] = 0.0;
+  const double2* ubf = ub + f * nq * R;
+  for (int d = 0; d < 26; ++d) {
+    int64_t qb[NT];
 #pragma unroll
-      for (int i = 0; i < NC; ++i) T[i] = tf[oid * NC + i];
-      const int lowmask = (1 << c) - 1;
+    for (int n = 0; n < NT; ++n) {
+      const int64_t Pn = P0 + n * 8 + g;
+      const int qq = Pn < npar ? nbr[Pn * 26 + d] : -1;
+      qb[n] = qq >= 0 ? (int64_t)qq * R + tq : -1;
+    }
+    {  // a direction none of the warp's parents has a (non-leaf) colleague in: no work
+      bool any = false;
 #pragma unroll
-      for (int q = 0; q < NPB; ++q) {
-        const int2 nb = s_nbr[q * 26 + dd];
-        if ((nb.y >> c) & 1) {
-          const int64_t s = nb.x + __popc(nb.y & lowmask);
-          if (KML == 1) {
-            cmac(acc[q][0], T[0], uhat[s * NF + fs]);
-          } else {
-            const double2 u0 = uhat[(s * 3 + 0) * NF + fs];
-            const double2 u1 = uhat[(s * 3 + 1) * NF + fs];
-            const double2 u2 = uhat[(s * 3 + 2) * NF + fs];
-            cmac(acc[q][0], T[0], u0);
-            cmac(acc[q][0], T[1], u1);
-            cmac(acc[q][0], T[2], u2);
-            cmac(acc[q][KML > 1 ? 1 : 0], T[1], u0);
-            cmac(acc[q][KML > 1 ? 1 : 0], T[3], u1);
-            cmac(acc[q][KML > 1 ? 1 : 0], T[4], u2);
-            cmac(acc[q][KML > 2 ? 2 : 0], T[2], u0);
-            cmac(acc[q][KML > 2 ? 2 : 0], T[4], u1);
-            cmac(acc[q][KML > 2 ? 2 : 0], T[5], u2);
-          }
+      for (int n = 0; n < NT; ++n) any |= qb[n] >= 0;
+      if (!__any_sync(0xffffffffu, any)) continue;
+    }
+    const int16_t* ai_tab = aidx + d * KS * KML * 32 + lane;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      double ar[KML], ai[KML], an[KML];
+#pragma unroll
+      for (int m = 0; m < KML; ++m) {
+        const int idx = ai_tab[(ks * KML + m) * 32];
+        const double2 t = idx >= 0 ? sT[idx] : make_double2(0.0, 0.0);
+        ar[m] = t.x;
+        ai[m] = t.y;
+        an[m] = -t.y;
+      }
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const double2 u = qb[n] >= 0 ? ubf[qb[n] + ks * 4] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int m = 0; m < KML; ++m) {
+          dmma(acc[m][n][0][0], acc[m][n][0][1], ar[m], u.x);
+          dmma(acc[m][n][0][0], acc[m][n][0][1], an[m], u.y);
+          dmma(acc[m][n][1][0], acc[m][n][1][1], ar[m], u.y);
+          dmma(acc[m][n][1][0], acc[m][n][1][1], ai[m], u.x);
         }
       }
     }
   }
-  if (!fok) return;
+  double2* cbf = cb + f * npar * R;
 #pragma unroll
-  for (int q = 0; q < NPB; ++q) {
-    const int2 pp = s_par[q];
-    if ((pp.y >> b) & 1) {
-      const int64_t t = pp.x + __popc(pp.y & ((1 << b) - 1));
+  for (int m = 0; m < KML; ++m)
 #pragma unroll
-      for (int a = 0; a < KML; ++a) chat[(t * KML + a) * NF + f] = acc[q][a];
-    }
-  }
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t Pn = P0 + n * 8 + 2 * tq + e;
+        if (Pn < npar) cbf[Pn * R + m * 8 + g] = make_double2(acc[m][n][0][e], acc[m][n][1][e]);
+      }
 }
 
 // ---------------------------------------------------------------------------
@@ -331,62 +360,55 @@ static void set_smem_attrs() {
 template <int P>
 static void launch_fwd(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
-  k_fft_fwd<P><<<(unsigned)ch.ns, 256, FftDims<P>::FWD_SMEM, Pl.stream>>>(ch.d_src, Pl.d_ue, Pl.ldn, Pl.kml,
-                                                                           Pl.d_lat, Pl.M, Pl.d_uhat);
+  k_fft_fwd<P><<<(unsigned)(8 * ch.nq), 256, FftDims<P>::FWD_SMEM, Pl.stream>>>(
+      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lat, Pl.M, Pl.d_ub);
   KF_CHECK_LAUNCH();
   Pl.launches++;
 }
 template <int P>
 static void launch_inv(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
-  k_fft_inv<P><<<(unsigned)ch.nt, 256, FftDims<P>::INV_SMEM, Pl.stream>>>(ch.t0, Pl.d_level, Pl.d_chat, Pl.kml,
-                                                                           Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn);
+  k_fft_inv<P><<<(unsigned)ch.nt, 256, FftDims<P>::INV_SMEM, Pl.stream>>>(
+      ch.d_tbox, ch.d_tpb, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn);
   KF_CHECK_LAUNCH();
   Pl.launches++;
 }
 
-static void dispatch_fwd(Plan& Pl, const FftChunk& ch) {
-  switch (Pl.p) {
-    case 4: launch_fwd<4>(Pl, ch); break;
-    case 5: launch_fwd<5>(Pl, ch); break;
-    case 6: launch_fwd<6>(Pl, ch); break;
-    case 7: launch_fwd<7>(Pl, ch); break;
-    case 8: launch_fwd<8>(Pl, ch); break;
-    case 10: launch_fwd<10>(Pl, ch); break;
-    case 12: launch_fwd<12>(Pl, ch); break;
-    default: throw Error{KAFMM_EINVAL, "FFT M2L: unsupported p"};
+#define KF_FFT_DISPATCH(FN)                                    \
+  switch (Pl.p) {                                              \
+    case 3: FN<3>(Pl, ch); break;                              \
+    case 4: FN<4>(Pl, ch); break;                              \
+    case 5: FN<5>(Pl, ch); break;                              \
+    case 6: FN<6>(Pl, ch); break;                              \
+    case 7: FN<7>(Pl, ch); break;                              \
+    case 8: FN<8>(Pl, ch); break;                              \
+    case 10: FN<10>(Pl, ch); break;                            \
+    case 12: FN<12>(Pl, ch); break;                            \
+    default: throw Error{KAFMM_EINVAL, "FFT M2L: unsupported p"}; \
   }
-}
-static void dispatch_inv(Plan& Pl, const FftChunk& ch) {
-  switch (Pl.p) {
-    case 4: launch_inv<4>(Pl, ch); break;
-    case 5: launch_inv<5>(Pl, ch); break;
-    case 6: launch_inv<6>(Pl, ch); break;
-    case 7: launch_inv<7>(Pl, ch); break;
-    case 8: launch_inv<8>(Pl, ch); break;
-    case 10: launch_inv<10>(Pl, ch); break;
-    case 12: launch_inv<12>(Pl, ch); break;
-    default: throw Error{KAFMM_EINVAL, "FFT M2L: unsupported p"};
-  }
-}
 
-bool fft_supported_p(int p) { return p == 4 || p == 5 || p == 6 || p == 7 || p == 8 || p == 10 || p == 12; }
+bool fft_supported_p(int p) { return (p >= 3 && p <= 8) || p == 10 || p == 12; }
+
+constexpr int NT_L = 8, NT_G = 4;  // parent n-tiles per warp (Laplace, Stokes family)
 
 void run_m2l_fft(Plan& Pl) {
   for (const FftChunk& ch : Pl.fft_chunks) {
-    if (ch.nt == 0 || ch.ns == 0) continue;
-    dispatch_fwd(Pl, ch);
-    const int nbp_1 = (int)((ch.npar + 15) / 16), nbp_3 = (int)((ch.npar + 3) / 4);
-    const int nfc = (Pl.NF + HAD_FPB - 1) / HAD_FPB;
+    if (ch.nt == 0 || ch.nq == 0) continue;
+    KF_FFT_DISPATCH(launch_fwd);
+    const int ppc = DM_WARPS * 8 * (Pl.kml == 1 ? NT_L : NT_G);
+    const int npb = (int)((ch.npar + ppc - 1) / ppc);
+    const unsigned grid = (unsigned)((int64_t)npb * Pl.NF);
+    prod_mark(Pl);
     if (Pl.kml == 1)
-      k_m2l_had<1, 16><<<(unsigned)((int64_t)nbp_1 * nfc), HAD_THREADS, 0, Pl.stream>>>(
-          Pl.NF, (int)ch.npar, Pl.d_that, Pl.d_uhat, Pl.d_chat, ch.d_par, ch.d_nbr);
+      k_m2l_dmma<1, NT_L><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb,
+                                                                 ch.d_nbr, Pl.d_aidx);
     else
-      k_m2l_had<3, 4><<<(unsigned)((int64_t)nbp_3 * nfc), HAD_THREADS, 0, Pl.stream>>>(
-          Pl.NF, (int)ch.npar, Pl.d_that, Pl.d_uhat, Pl.d_chat, ch.d_par, ch.d_nbr);
+      k_m2l_dmma<3, NT_G><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb,
+                                                                 ch.d_nbr, Pl.d_aidx);
     KF_CHECK_LAUNCH();
+    prod_mark(Pl);
     Pl.launches++;
-    dispatch_inv(Pl, ch);
+    KF_FFT_DISPATCH(launch_inv);
   }
 }
 
@@ -402,11 +424,11 @@ void build_fft_m2l(Plan& P, int64_t budget) {
     return;
   }
   cudaStream_t st = P.stream;
-  const int p = P.p;
-  P.NG = 2 * p;
-  P.NZ = p + 1;
+  const int p = P.p, kml = P.kml, R = 8 * kml;
+  P.NG = 2 * p - 1;
+  P.NZ = P.NG / 2 + 1;
   P.NF = P.NG * P.NG * P.NZ;
-  P.ncomp = P.kml == 1 ? 1 : 6;
+  P.ncomp = kml == 1 ? 1 : 6;
   // offset table (same enumeration as the list builder and the dense operators)
   int16_t tab[343];
   std::vector<int8_t> offs;
@@ -422,7 +444,32 @@ void build_fft_m2l(Plan& P, int64_t budget) {
       tab[a] = -1;
     }
   }
-  KF_CUDA(cudaMemcpyToSymbol(c_fft_off_id, tab, sizeof(tab)));
+  // DMMA A-fragment table: for direction d, k-step ks, m-tile m and lane, the
+  // shared-memory index of T_o[sym(a, e)] (or -1 where the child pair is adjacent)
+  {
+    const int KS = R / 4, NC = P.ncomp;
+    const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+    std::vector<int16_t> ai((size_t)26 * KS * kml * 32);
+    for (int dd = 0; dd < 26; ++dd) {
+      const int d = dd < 13 ? dd : dd + 1;
+      const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
+      for (int ks = 0; ks < KS; ++ks)
+        for (int m = 0; m < kml; ++m)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int row = m * 8 + (lane >> 2), k = ks * 4 + (lane & 3);
+            const int b = row / kml, a = row % kml, c = k / kml, e = k % kml;
+            const int ox = 2 * dx + ((c >> 2) & 1) - ((b >> 2) & 1);
+            const int oy = 2 * dy + ((c >> 1) & 1) - ((b >> 1) & 1);
+            const int oz = 2 * dz + (c & 1) - (b & 1);
+            int v = -1;
+            if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) >= 2)
+              v = tab[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)] * NC + (kml == 1 ? 0 : sym[a][e]);
+            ai[((size_t)(dd * KS + ks) * kml + m) * 32 + lane] = (int16_t)v;
+          }
+    }
+    P.d_aidx = dalloc<int16_t>(P, ai.size());
+    KF_CUDA(cudaMemcpyAsync(P.d_aidx, ai.data(), ai.size() * 2, cudaMemcpyHostToDevice, st));
+  }
   // integer lattice of the surface points (same order as d_surf)
   std::vector<int16_t> lat;
   for (int i = 0; i < p; ++i)
@@ -446,7 +493,7 @@ void build_fft_m2l(Plan& P, int64_t budget) {
     KF_CUDA(cudaMalloc(&grid, (size_t)N_OFFSETS * nc * NG3 * 8));
     KF_CUDA(cudaMalloc(&spec, (size_t)N_OFFSETS * nc * P.NF * 16));
     dim3 g(nblk(NG3), N_OFFSETS);
-    k_kernel_grid<<<g, 256, 0, st>>>(p, NG, P.kml, 1.05 / (p - 1), d_offs, grid);
+    k_kernel_grid<<<g, 256, 0, st>>>(p, NG, kml, 1.05 / (p - 1), d_offs, grid);
     KF_CHECK_LAUNCH();
     cufftHandle h;
     int n[3] = {NG, NG, NG};
@@ -464,7 +511,16 @@ void build_fft_m2l(Plan& P, int64_t budget) {
     cudaFree(spec);
     cudaFree(d_offs);
   }
-  // chunks: per level l >= 2, Morton-contiguous target parents at level l-1
+  build_fft_chunks(P, budget);
+}
+
+// chunks: per level l >= 2, Morton-contiguous runs of target parents at level
+// l-1 (only parents whose subtree is active on this rank), sized to the budget
+void build_fft_chunks(Plan& P, int64_t budget) {
+  if (P.NF == 0) return;
+  cudaStream_t st = P.stream;
+  const int R = 8 * P.kml;
+  P.fft_budget = budget;
   std::vector<int32_t> child, ijk;
   std::vector<uint8_t> leaf;
   std::vector<uint64_t> key;
@@ -482,112 +538,78 @@ void build_fft_m2l(Plan& P, int64_t budget) {
     auto it = std::lower_bound(b, e, kk);
     return (it != e && *it == kk) ? (int64_t)(it - key.begin()) : -1;
   };
-  const int64_t per_box = (int64_t)P.kml * P.NF * 16;
+  const int64_t per_block = (int64_t)R * P.NF * 16;  // one parent block of spectra
   P.fft_chunks.clear();
-  P.fft_max_ns = P.fft_max_nt = 0;
+  P.fft_max_nq = P.fft_max_npar = 0;
+  std::vector<int32_t> qlocal(P.nbox, -1);
   for (int l = 2; l <= P.depth; ++l) {
-    const int64_t lb = P.levels[l].begin, le = P.levels[l].end;
-    std::vector<int32_t> local(le - lb, -1);
     std::vector<int64_t> parents;
     for (int64_t b = P.levels[l - 1].begin; b < P.levels[l - 1].end; ++b)
-      if (!leaf[b]) parents.push_back(b);
+      if (!leaf[b] && (P.box_active.empty() || P.box_active[b])) parents.push_back(b);
     size_t i0 = 0;
     while (i0 < parents.size()) {
-      // grow the chunk until the source + target spectra exceed the budget
-      std::vector<int64_t> nbrs;  // (26 per parent) colleague ids or -1
-      std::vector<int32_t> srcs;
-      int64_t nt = 0;
+      std::vector<int32_t> qs, nb;
       size_t i1 = i0;
       while (i1 < parents.size()) {
         const int64_t Pb = parents[i1];
-        int64_t add_src = 0;
-        int64_t qs[26];
+        int64_t cq[26];
+        int add = 0;
         for (int dd = 0; dd < 26; ++dd) {
           int d = dd < 13 ? dd : dd + 1;
-          int64_t q = find(l - 1, ijk[3 * Pb] + d / 9 - 1, ijk[3 * Pb + 1] + (d / 3) % 3 - 1, ijk[3 * Pb + 2] + d % 3 - 1);
+          int64_t q = find(l - 1, ijk[3 * Pb] + d / 9 - 1, ijk[3 * Pb + 1] + (d / 3) % 3 - 1,
+                           ijk[3 * Pb + 2] + d % 3 - 1);
           if (q >= 0 && leaf[q]) q = -1;
-          qs[dd] = q;
-          if (q >= 0) {
-            int64_t c0 = -1;
-            for (int o = 0; o < 8; ++o)
-              if (child[8 * q + o] >= 0) {
-                c0 = child[8 * q + o];
-                break;
-              }
-            if (local[c0 - lb] < 0) {
-              for (int o = 0; o < 8; ++o) add_src += child[8 * q + o] >= 0;
-            }
-          }
+          cq[dd] = q;
+          if (q >= 0 && qlocal[q] < 0) ++add;
         }
-        int64_t add_t = 0;
-        for (int o = 0; o < 8; ++o) add_t += child[8 * Pb + o] >= 0;
-        if (i1 > i0 && ((int64_t)srcs.size() + add_src + nt + add_t) * per_box > budget) break;
+        if (i1 > i0 && ((int64_t)qs.size() + add + (int64_t)(i1 - i0) + 1) * per_block > budget) break;
         for (int dd = 0; dd < 26; ++dd) {
-          int64_t q = qs[dd];
-          nbrs.push_back(q);
-          if (q >= 0) {
-            for (int o = 0; o < 8; ++o) {
-              int64_t c = child[8 * q + o];
-              if (c >= 0 && local[c - lb] < 0) {
-                local[c - lb] = 0;  // mark; final local indices after sorting
-                srcs.push_back((int32_t)c);
-              }
-            }
+          const int64_t q = cq[dd];
+          if (q >= 0 && qlocal[q] < 0) {
+            qlocal[q] = (int32_t)qs.size();
+            qs.push_back((int32_t)q);
           }
+          nb.push_back(q >= 0 ? qlocal[q] : -1);
         }
-        nt += add_t;
         ++i1;
       }
-      std::sort(srcs.begin(), srcs.end());
-      for (size_t s = 0; s < srcs.size(); ++s) local[srcs[s] - lb] = (int32_t)s;
       FftChunk ch;
       ch.level = l;
       ch.npar = (int64_t)(i1 - i0);
-      ch.ns = (int64_t)srcs.size();
-      ch.nt = nt;
-      // targets: children of parents[i0..i1) form one contiguous id range
-      int64_t t0 = -1;
-      for (int o = 0; o < 8 && t0 < 0; ++o)
-        if (child[8 * parents[i0] + o] >= 0) t0 = child[8 * parents[i0] + o];
-      ch.t0 = t0;
-      std::vector<int2> hpar(ch.npar), hnbr(ch.npar * 26);
-      for (int64_t q = 0; q < ch.npar; ++q) {
-        const int64_t Pb = parents[i0 + q];
-        int mask = 0, first = -1;
-        for (int o = 0; o < 8; ++o)
-          if (child[8 * Pb + o] >= 0) {
-            mask |= 1 << o;
-            if (first < 0) first = child[8 * Pb + o];
+      ch.nq = (int64_t)qs.size();
+      std::vector<int32_t> tb;
+      std::vector<int2> tpb;
+      for (int64_t q = 0; q < ch.npar; ++q)
+        for (int o = 0; o < 8; ++o) {
+          const int32_t c = child[8 * parents[i0 + q] + o];
+          if (c >= 0 && (P.box_active.empty() || P.box_active[c])) {
+            tb.push_back(c);
+            tpb.push_back(make_int2((int)q, o));
           }
-        hpar[q] = make_int2((int)(first - t0), mask);
-        for (int dd = 0; dd < 26; ++dd) {
-          int64_t Q = nbrs[q * 26 + dd];
-          int m2 = 0, f2 = -1;
-          if (Q >= 0)
-            for (int o = 0; o < 8; ++o)
-              if (child[8 * Q + o] >= 0) {
-                m2 |= 1 << o;
-                if (f2 < 0) f2 = child[8 * Q + o];
-              }
-          hnbr[q * 26 + dd] = (Q >= 0) ? make_int2(local[f2 - lb], m2) : make_int2(0, 0);
         }
+      ch.nt = (int64_t)tb.size();
+      ch.d_qbox = dalloc<int32_t>(P, std::max<int64_t>(1, ch.nq));
+      ch.d_nbr = dalloc<int32_t>(P, ch.npar * 26);
+      ch.d_tbox = dalloc<int32_t>(P, std::max<int64_t>(1, ch.nt));
+      ch.d_tpb = dalloc<int2>(P, std::max<int64_t>(1, ch.nt));
+      if (ch.nq) KF_CUDA(cudaMemcpyAsync(ch.d_qbox, qs.data(), ch.nq * 4, cudaMemcpyHostToDevice, st));
+      KF_CUDA(cudaMemcpyAsync(ch.d_nbr, nb.data(), ch.npar * 26 * 4, cudaMemcpyHostToDevice, st));
+      if (ch.nt) {
+        KF_CUDA(cudaMemcpyAsync(ch.d_tbox, tb.data(), ch.nt * 4, cudaMemcpyHostToDevice, st));
+        KF_CUDA(cudaMemcpyAsync(ch.d_tpb, tpb.data(), ch.nt * 8, cudaMemcpyHostToDevice, st));
       }
-      ch.d_src = dalloc<int32_t>(P, std::max<int64_t>(1, ch.ns));
-      ch.d_par = dalloc<int2>(P, ch.npar);
-      ch.d_nbr = dalloc<int2>(P, ch.npar * 26);
-      if (ch.ns) KF_CUDA(cudaMemcpyAsync(ch.d_src, srcs.data(), ch.ns * 4, cudaMemcpyHostToDevice, st));
-      KF_CUDA(cudaMemcpyAsync(ch.d_par, hpar.data(), ch.npar * 8, cudaMemcpyHostToDevice, st));
-      KF_CUDA(cudaMemcpyAsync(ch.d_nbr, hnbr.data(), ch.npar * 26 * 8, cudaMemcpyHostToDevice, st));
       KF_CUDA(cudaStreamSynchronize(st));
-      for (int32_t s : srcs) local[s - lb] = -1;
-      P.fft_max_ns = std::max(P.fft_max_ns, ch.ns);
-      P.fft_max_nt = std::max(P.fft_max_nt, ch.nt);
+      for (int32_t q : qs) qlocal[q] = -1;
+      P.fft_max_nq = std::max(P.fft_max_nq, ch.nq);
+      P.fft_max_npar = std::max(P.fft_max_npar, ch.npar);
       P.fft_chunks.push_back(ch);
       i0 = i1;
     }
   }
-  P.d_uhat = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_ns) * P.kml * P.NF);
-  P.d_chat = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_nt) * P.kml * P.NF);
+  dfree(P, P.d_ub);
+  dfree(P, P.d_cb);
+  P.d_ub = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_nq) * R * P.NF);
+  P.d_cb = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_npar) * R * P.NF);
 }
 
 }  // namespace kafmm

@@ -47,23 +47,44 @@ struct LevelRange {
   int64_t begin, end;  // box ids [begin, end) of one level
 };
 
-// FFT M2L work unit: a Morton-contiguous range of target parents at level-1,
-// its target boxes (their children, a contiguous id range) and the source
-// boxes (children of the parents' colleagues), sized to a memory budget.
+// FFT M2L work unit (kafmm_fft.cu): a Morton-contiguous run of target parents
+// at level-1 (non-leaf), their children (the M2L targets) and the source
+// parents Q (non-leaf colleagues of the target parents, whose children are
+// the sources), sized to a memory budget.
 struct FftChunk {
   int level = 0;
-  int64_t npar = 0, ns = 0, nt = 0;
-  int64_t t0 = 0;            // first target box id; local target t = id - t0
-  int32_t* d_src = nullptr;  // ns source box ids (sorted)
-  int2* d_nbr = nullptr;     // npar x 26: (local index of the colleague's first child, child mask)
-  int2* d_par = nullptr;     // npar: (local index of the parent's first child, child mask)
+  int64_t npar = 0, nq = 0, nt = 0;
+  int32_t* d_qbox = nullptr;  // nq source parent box ids
+  int32_t* d_nbr = nullptr;   // npar x 26: local q of the colleague in direction d, or -1
+  int32_t* d_tbox = nullptr;  // nt target box ids
+  int2* d_tpb = nullptr;      // nt: (local parent index, child octant)
 };
 
 enum M2LMode { M2L_DENSE = 0, M2L_FFT = 1 };
 
+// The work lists the evaluation kernels run over.  For a plan built by
+// kafmm_setup they alias the full lists; kafmm_restrict (multi-GPU, one rank
+// per GPU) replaces them with the part of the tree this rank owns.
+struct Jobs {
+  int64_t plo = 0, phi = 0;          // owned points, Morton (sorted) order
+  int32_t* leaf_ids = nullptr;       // owned leaves (L2T, M2T, P2P jobs)
+  int64_t nleaf = 0;
+  int64_t* w_off = nullptr;          // W list per job (CSR)
+  int32_t* w_src = nullptr;
+  int64_t* u_roff = nullptr;         // P2P merged source ranges per job (CSR)
+  int2* u_rng = nullptr;
+  int32_t* s2m_ids = nullptr;        // owned leaves at level >= 2
+  int64_t ns2m = 0;
+  int32_t* x_tgt = nullptr;          // active boxes with a non-empty X list
+  int64_t nx = 0;
+  int64_t* x_roff = nullptr;
+  int2* x_rng = nullptr;
+};
+
 enum Stage {
   ST_GATHER = 0, ST_S2M, ST_UC2UE, ST_M2M, ST_M2L, ST_S2L, ST_DC2DE, ST_L2L,
-  ST_LEAF_FAR, ST_P2P, ST_SCATTER, ST_TOTAL
+  ST_LEAF_FAR, ST_P2P, ST_SCATTER, ST_TOTAL,
+  ST_M2L_PRODUCT  // reported only: device time of the M2L product kernels (part of ST_M2L)
 };
 
 struct Plan {
@@ -78,13 +99,17 @@ struct Plan {
   cudaStream_t stream = 0;
   bool timing = false;
   cudaEvent_t ev[ST_TOTAL + 1] = {};
-  float stage_ms[ST_TOTAL + 1] = {};
+  float stage_ms[ST_M2L_PRODUCT + 1] = {};
+  std::vector<cudaEvent_t> prod_ev;  // start/stop pairs around the M2L product launches (timing on)
+  int prod_used = 0;
   int launches = 0;
 
   // tree (device unless noted)
   int depth = 0;
   int64_t nbox = 0, nleaf = 0;
   std::vector<LevelRange> levels;  // host
+  std::vector<uint8_t> box_active; // host; empty = every box (single plan), else the
+                                   // boxes whose subtree holds points of this rank
   int32_t* d_level = nullptr;
   int32_t* d_ijk = nullptr;        // 3 per box
   int32_t* d_parent = nullptr;
@@ -105,6 +130,10 @@ struct Plan {
   int64_t n_u = 0, n_w = 0, n_v = 0, n_p2p = 0;
   int32_t* d_s2m_ids = nullptr;    // leaves at level >= 2 (S2M jobs)
   int64_t n_s2m = 0;
+  int2* d_u_rng = nullptr;         // P2P: merged source point ranges [x, y) per leaf slot
+  int64_t* d_u_roff = nullptr;     // (CSR offsets, nleaf + 1)
+  int2* d_x_rng = nullptr;         // S2L: merged source point ranges per X target
+  int64_t* d_x_roff = nullptr;     // (CSR offsets, n_xbox + 1)
   int32_t* d_x_tgt = nullptr;      // boxes with a non-empty X list
   int64_t* d_x_off = nullptr;
   int32_t* d_x_src = nullptr;
@@ -124,16 +153,20 @@ struct Plan {
   int rows_pad = 0;                // neq rounded up to GEMM_BM
   std::vector<double> h_sigma;
 
-  // FFT M2L (convolution on the (2p)^3 lattice grid)
+  // FFT M2L (convolution on the NG^3 lattice grid, NG = 2p - 1)
   int m2l_mode = M2L_FFT;
-  int NG = 0, NZ = 0, NF = 0;      // grid 2p, half-spectrum p+1, bins NG*NG*NZ
+  int NG = 0, NZ = 0, NF = 0;      // grid, half-spectrum NG/2+1, bins NG*NG*NZ
   int ncomp = 0;                   // stored components per operator spectrum: 1 (L) or 6 (sym. G)
   double2* d_that = nullptr;       // [NF][316][ncomp] operator spectra at level 0
   int16_t* d_lat = nullptr;        // M x 3 integer lattice coordinates of the surface points
+  int16_t* d_aidx = nullptr;       // DMMA A-fragment gather table [26][8kml/4][kml][32]
   std::vector<FftChunk> fft_chunks;
-  double2* d_uhat = nullptr;       // [max_ns][kml][NF]
-  double2* d_chat = nullptr;       // [max_nt][kml][NF]
-  int64_t fft_max_ns = 0, fft_max_nt = 0;
+  double2* d_ub = nullptr;         // [NF][nq][8 kml] source spectra by parent block
+  double2* d_cb = nullptr;         // [NF][npar][8 kml] target check spectra by parent block
+  int64_t fft_max_nq = 0, fft_max_npar = 0, fft_budget = 0;
+
+  Jobs J;
+  bool restricted = false;
 
   // GEMM batches
   GemmBatch g_uc2ue_1, g_uc2ue_2;              // S2M leaves (level >= 2)
@@ -183,6 +216,27 @@ T* dalloc(Plan& P, size_t count) {
   return (T*)p;
 }
 
+// release a dalloc'ed buffer early (re-planning after kafmm_restrict)
+inline void dfree(Plan& P, void* p) {
+  if (!p) return;
+  for (auto& a : P.allocs)
+    if (a == p) {
+      cudaFree(p);
+      a = nullptr;
+    }
+}
+
+// event around an M2L product launch (stage timing only)
+inline void prod_mark(Plan& P) {
+  if (!P.timing) return;
+  if ((int)P.prod_ev.size() <= P.prod_used) {
+    cudaEvent_t e;
+    KF_CUDA(cudaEventCreate(&e));
+    P.prod_ev.push_back(e);
+  }
+  KF_CUDA(cudaEventRecord(P.prod_ev[P.prod_used++], P.stream));
+}
+
 inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 // translation units
@@ -191,10 +245,19 @@ void build_operators(Plan& P);                               // kafmm_ops.cu
 void build_gemm_batches(Plan& P);                            // kafmm_tree.cu
 void upload_batch(Plan& P, GemmBatch& g, const std::vector<int2>& h_items);
 void run_eval(Plan& P, const double* d_src, double* d_out);  // kafmm_eval.cu
+void run_eval_up(Plan& P, const double* d_src);               // a1-a4
+void run_eval_down(Plan& P, double* d_out);                   // a5-a12
+void restrict_plan(Plan& P, int64_t plo, int64_t phi);        // kafmm_dist.cu
+void build_m2l_batch(Plan& P);                                // kafmm_dist.cu
+void pack_ue(Plan& P, const int32_t* ids, int64_t n, double* buf);
+void unpack_ue(Plan& P, const int32_t* ids, int64_t n, const double* buf);
+void gather_rows(Plan& P, const double* src, int ld, const int64_t* idx, int64_t n, double* dst);
+void scatter_rows(Plan& P, const double* src, int ld, const int64_t* idx, int64_t n, double* dst);
 void check_values(Plan& P, const double* d_src);             // kafmm_eval.cu
 void launch_gemm(Plan& P, const GemmBatch& g, const double* A, int M, int K, int lda,
                  const double* B, int ldb, double* C, int ldc, int mode);  // kafmm_gemm.cu
 void build_fft_m2l(Plan& P, int64_t budget_bytes);           // kafmm_fft.cu
+void build_fft_chunks(Plan& P, int64_t budget_bytes);        // kafmm_fft.cu
 void run_m2l_fft(Plan& P);                                   // kafmm_fft.cu
 
 }  // namespace kafmm

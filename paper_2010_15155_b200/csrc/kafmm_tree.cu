@@ -326,6 +326,29 @@ static void exclusive_scan(Plan& P, const int64_t* in, int64_t* out, int64_t n) 
   KF_CUDA(cudaFreeAsync(d_tmp, P.stream));
 }
 
+// per job s: the point ranges [pbeg, pend) of boxes src[off[s] .. off[s+1]),
+// sorted and merged where they touch
+static void merged_ranges(const std::vector<int64_t>& off, const std::vector<int32_t>& src,
+                          const std::vector<int64_t>& pb, const std::vector<int64_t>& pe, int64_t njobs,
+                          std::vector<int2>& rng, std::vector<int64_t>& roff) {
+  rng.clear();
+  roff.assign(1, 0);
+  std::vector<int2> tmp;
+  for (int64_t s = 0; s < njobs; ++s) {
+    tmp.clear();
+    for (int64_t e = off[s]; e < off[s + 1]; ++e) {
+      const int32_t b = src[e];
+      if (pe[b] > pb[b]) tmp.push_back(make_int2((int)pb[b], (int)pe[b]));
+    }
+    std::sort(tmp.begin(), tmp.end(), [](int2 a, int2 b) { return a.x < b.x; });
+    for (size_t i = 0; i < tmp.size(); ++i) {
+      if (i > 0 && rng.back().y == tmp[i].x) rng.back().y = tmp[i].y;
+      else rng.push_back(tmp[i]);
+    }
+    roff.push_back((int64_t)rng.size());
+  }
+}
+
 void build_tree_and_lists(Plan& P, const double* d_points) {
   const int64_t n = P.n;
   cudaStream_t st = P.stream;
@@ -631,7 +654,45 @@ void build_tree_and_lists(Plan& P, const double* d_points) {
       tot += nt * ns;
     }
     P.n_p2p = tot;
+    // merged source point ranges of the P2P (U) and S2L (X) streams: the
+    // sources of adjacent Morton leaves are contiguous in the sorted points
+    std::vector<int2> rng;
+    std::vector<int64_t> roff;
+    merged_ranges(uoff, usrc, pb, pe, P.nleaf, rng, roff);
+    P.d_u_rng = dalloc<int2>(P, std::max<size_t>(1, rng.size()));
+    P.d_u_roff = dalloc<int64_t>(P, roff.size());
+    if (!rng.empty()) KF_CUDA(cudaMemcpyAsync(P.d_u_rng, rng.data(), rng.size() * 8, cudaMemcpyHostToDevice, st));
+    KF_CUDA(cudaMemcpyAsync(P.d_u_roff, roff.data(), roff.size() * 8, cudaMemcpyHostToDevice, st));
+    KF_CUDA(cudaStreamSynchronize(st));
+    if (P.n_xbox > 0) {
+      std::vector<int64_t> xoff;
+      std::vector<int32_t> xsrc;
+      to_host(P, xoff, P.d_x_off, P.n_xbox + 1);
+      to_host(P, xsrc, P.d_x_src, P.n_w);
+      merged_ranges(xoff, xsrc, pb, pe, P.n_xbox, rng, roff);
+      P.d_x_rng = dalloc<int2>(P, std::max<size_t>(1, rng.size()));
+      P.d_x_roff = dalloc<int64_t>(P, roff.size());
+      if (!rng.empty()) KF_CUDA(cudaMemcpyAsync(P.d_x_rng, rng.data(), rng.size() * 8, cudaMemcpyHostToDevice, st));
+      KF_CUDA(cudaMemcpyAsync(P.d_x_roff, roff.data(), roff.size() * 8, cudaMemcpyHostToDevice, st));
+      KF_CUDA(cudaStreamSynchronize(st));
+    }
   }
+  // the evaluation runs over every box until kafmm_restrict narrows it
+  Jobs& J = P.J;
+  J.plo = 0;
+  J.phi = P.n;
+  J.leaf_ids = P.d_leaf_ids;
+  J.nleaf = P.nleaf;
+  J.w_off = P.d_w_off;
+  J.w_src = P.d_w_src;
+  J.u_roff = P.d_u_roff;
+  J.u_rng = P.d_u_rng;
+  J.s2m_ids = P.d_s2m_ids;
+  J.ns2m = P.n_s2m;
+  J.x_tgt = P.d_x_tgt;
+  J.nx = P.n_xbox;
+  J.x_roff = P.d_x_roff;
+  J.x_rng = P.d_x_rng;
 }
 
 // GEMM work lists of the per-box translations -----------------------------
@@ -667,8 +728,9 @@ void build_gemm_batches(Plan& P) {
   to_host(P, hlevel, P.d_level, P.nbox);
   to_host(P, hparent, P.d_parent, P.nbox);
   to_host(P, hijk, P.d_ijk, 3 * P.nbox);
-  to_host(P, hs2m, P.d_s2m_ids, P.n_s2m);
+  to_host(P, hs2m, P.J.s2m_ids, P.J.ns2m);
   auto oct = [&](int64_t b) { return 4 * (hijk[3 * b] & 1) + 2 * (hijk[3 * b + 1] & 1) + (hijk[3 * b + 2] & 1); };
+  auto act = [&](int64_t b) { return P.box_active.empty() || P.box_active[b] != 0; };
   // UC2UE on the S2M leaves (level >= 2), level-major so alpha = 2^-l forms runs
   {
     std::vector<int2> it;
@@ -690,7 +752,7 @@ void build_gemm_batches(Plan& P) {
   for (int l = P.depth - 1; l >= 2; --l) {
     std::vector<std::vector<int2>> by(8);
     for (int64_t c = P.levels[l + 1].begin; c < P.levels[l + 1].end; ++c)
-      by[oct(c)].push_back(make_int2((int)c, hparent[c]));
+      if (act(c)) by[oct(c)].push_back(make_int2((int)c, hparent[c]));
     std::vector<int2> it;
     std::vector<int> op;
     std::vector<double> al;
@@ -714,6 +776,7 @@ void build_gemm_batches(Plan& P) {
     std::vector<int> op;
     std::vector<double> a1, a2;
     for (int64_t b = P.levels[l].begin; b < P.levels[l].end; ++b) {
+      if (!act(b)) continue;
       it.push_back(make_int2((int)b, (int)b));
       op.push_back(0);
       a1.push_back(1.0);
@@ -729,7 +792,8 @@ void build_gemm_batches(Plan& P) {
     GemmBatch g3;
     if (l >= 3) {
       std::vector<std::vector<int2>> by(8);
-      for (int64_t b = P.levels[l].begin; b < P.levels[l].end; ++b) by[oct(b)].push_back(make_int2(hparent[b], (int)b));
+      for (int64_t b = P.levels[l].begin; b < P.levels[l].end; ++b)
+        if (act(b)) by[oct(b)].push_back(make_int2(hparent[b], (int)b));
       std::vector<int2> it3;
       std::vector<int> op3;
       std::vector<double> al3;

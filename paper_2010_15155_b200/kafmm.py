@@ -13,7 +13,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 KERNELS = {"laplace_pgrad": 1, "stokeslet": 2, "rpy": 3, "stokes_reg_vel": 4}
-N_STAGES = 12
+N_STAGES = 13
 
 
 class KafmmError(RuntimeError):
@@ -63,6 +63,13 @@ _SIGS = [
     ("kafmm_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     ("kafmm_set_m2l_mode", C.c_int, [C.c_void_p, C.c_int]),
     ("kafmm_get_m2l_mode", C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+    ("kafmm_restrict", C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
+    ("kafmm_eval_up", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kafmm_eval_down", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kafmm_pack_ue", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("kafmm_unpack_ue", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("kafmm_gather_rows", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("kafmm_scatter_rows", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
 ]
 EXPORTED = [s[0] for s in _SIGS]
 
@@ -223,6 +230,34 @@ class KAFMM:
         m = C.c_int()
         _check(self.lib.kafmm_get_m2l_mode(self.h, C.byref(m)), "kafmm_get_m2l_mode")
         return ["dense", "fft"][m.value]
+
+    # multi-GPU building blocks (dist.py)
+    def restrict(self, plo: int, phi: int):
+        _check(self.lib.kafmm_restrict(self.h, int(plo), int(phi)), "kafmm_restrict")
+
+    def eval_up(self, src):
+        _check(self.lib.kafmm_eval_up(self.h, C.c_void_p(src.data_ptr())), "kafmm_eval_up")
+
+    def eval_down(self, out):
+        _check(self.lib.kafmm_eval_down(self.h, C.c_void_p(out.data_ptr())), "kafmm_eval_down")
+
+    def pack_ue(self, ids, buf):
+        _check(self.lib.kafmm_pack_ue(self.h, C.c_void_p(ids.data_ptr()), int(ids.numel()),
+                                      C.c_void_p(buf.data_ptr())), "kafmm_pack_ue")
+
+    def unpack_ue(self, ids, buf):
+        _check(self.lib.kafmm_unpack_ue(self.h, C.c_void_p(ids.data_ptr()), int(ids.numel()),
+                                        C.c_void_p(buf.data_ptr())), "kafmm_unpack_ue")
+
+    def gather_rows(self, src, idx, dst):
+        _check(self.lib.kafmm_gather_rows(self.h, C.c_void_p(src.data_ptr()), int(src.shape[1]),
+                                          C.c_void_p(idx.data_ptr()), int(idx.numel()), C.c_void_p(dst.data_ptr())),
+               "kafmm_gather_rows")
+
+    def scatter_rows(self, src, idx, dst):
+        _check(self.lib.kafmm_scatter_rows(self.h, C.c_void_p(src.data_ptr()), int(dst.shape[1]),
+                                           C.c_void_p(idx.data_ptr()), int(idx.numel()), C.c_void_p(dst.data_ptr())),
+               "kafmm_scatter_rows")
 
     def launch_count(self) -> int:
         n = C.c_int()
