@@ -11,9 +11,10 @@ in HBM.  L2 is flushed (256 MiB write) before every timed step, outside the
 timed interval; each step is bracketed by CUDA events on the plan's stream.
 "e2e" times kafmm_eval_host: pinned host values -> device, eval, -> host.
 
-Multi-GPU (torchrun, N > 1): every rank evaluates its own instance of the
-workload (weak scaling, no data-path collective); the Morton-partitioned
-single-problem path is listed as NEXT in DESIGN.md.  Time = max over ranks.
+Multi-GPU (torchrun, N > 1): ONE problem split into contiguous Morton ranges
+(paper_2010_15155_b200.dist): every rank holds a slice of the user rows,
+the ranks exchange source values, shared and ghost multipoles and outputs
+over NCCL (strong scaling).  Time = max over ranks.
 
 --impl reference times the CPU oracle (oracle/, test infrastructure) on a
 bounded sample of the same workload on the host cores (rank 0 only).
@@ -180,7 +181,7 @@ def run_reference(args, spec, pts, vals, rank):
     cores = len(os.sched_getaffinity(0))
     line = {"impl": "reference", "metric": "FMM eval points/sec (N_S+N_T) at fixed p", "value": value,
             "unit": "points/s", "n_gpus": args.gpus, "steps": len(per), "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(spec), "kernel": spec.kernel, "n": spec.n, "p": spec.p,
                        "max_pts_per_leaf": spec.cap},
@@ -216,10 +217,33 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
-    plan = KAFMM(spec_pts, spec.kernel, spec.p, spec.cap, stream=stream)
-    info = plan.info()
-    src = torch.from_numpy(vals).cuda()
-    out = torch.empty((spec.n, info.k_t), dtype=torch.float64, device="cuda")
+    if world == 1:
+        # one GPU: the whole evaluation through kafmm_eval
+        plan = KAFMM(spec_pts, spec.kernel, spec.p, spec.cap, stream=stream)
+        info = plan.info()
+        src = torch.from_numpy(vals).cuda()
+        out = torch.empty((spec.n, info.k_t), dtype=torch.float64, device="cuda")
+        run_step = lambda: plan.eval(src, out)  # noqa: E731
+        n_v_local, n_p2p_local = info.n_v_pairs, info.n_p2p
+        h_vals = vals
+        def run_e2e(hsrc, hout):
+            plan.eval_host(hsrc, hout)
+    else:
+        # N GPUs: ONE problem split by Morton ranges (strong scaling); every rank
+        # holds a contiguous slice of the user rows and gets its rows' outputs back
+        from paper_2010_15155_b200.dist import DistKAFMM
+        offs = np.linspace(0, spec.n, world + 1).astype(np.int64)
+        lo, hi = int(offs[rank]), int(offs[rank + 1])
+        dk = DistKAFMM(spec_pts[lo:hi], spec.kernel, spec.p, spec.cap, stream=stream)
+        plan = dk.ctx.plan
+        info = plan.info()
+        h_vals = np.ascontiguousarray(vals[lo:hi])
+        src = torch.from_numpy(h_vals).cuda()
+        run_step = lambda: dk.eval(src)  # noqa: E731
+        n_v_local, n_p2p_local = dk.ctx.work["n_v"], dk.ctx.work["n_p2p"]
+        def run_e2e(hsrc, hout):
+            o = dk.eval(torch.from_numpy(hsrc).cuda(non_blocking=True))
+            hout[...] = o.cpu().numpy()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
@@ -228,7 +252,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        plan.eval(src, out)
+        run_step()
     barrier()
 
     plan.set_timing(True)  # per-stage CUDA events on the plan's stream
@@ -237,11 +261,11 @@ def main():
         barrier()
         for _ in range(args.steps):
             flush.fill_(1.0)
-            torch.cuda.synchronize()
+            barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            plan.eval(src, out)
+            run_step()
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -255,26 +279,26 @@ def main():
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms = float(tot.item()) / args.steps
-    value = world * 2 * spec.n / (ms * 1e-3)
+    value = 2 * spec.n / (ms * 1e-3)   # the whole job: one problem of N_S + N_T = 2N points
 
-    # e2e through the public API with host buffers
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        hsrc = torch.from_numpy(vals).pin_memory().numpy()
-        hout = torch.empty((spec.n, info.k_t), dtype=torch.float64).pin_memory().numpy()
-        plan.eval_host(hsrc, hout)
+        hsrc = torch.from_numpy(h_vals).pin_memory().numpy()
+        hout = torch.empty((h_vals.shape[0], info.k_t), dtype=torch.float64).pin_memory().numpy()
+        run_e2e(hsrc, hout)
         et = []
         for _ in range(args.steps):
             barrier()
             t0 = time.perf_counter()
-            plan.eval_host(hsrc, hout)
+            run_e2e(hsrc, hout)
             et.append(time.perf_counter() - t0)
         e = torch.tensor([sum(et)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(e, op=dist.ReduceOp.MAX)
         e_s = float(e.item()) / args.steps
-        e2e = {"value": world * 2 * spec.n / e_s, "unit": "points/s", "ms_per_step": 1e3 * e_s,
-               "h2d_bytes_per_step": int(vals.nbytes), "d2h_bytes_per_step": int(hout.nbytes)}
+        e2e = {"value": 2 * spec.n / e_s, "unit": "points/s", "ms_per_step": 1e3 * e_s,
+               "h2d_bytes_per_step": int(hsrc.nbytes) * world, "d2h_bytes_per_step": int(hout.nbytes) * world}
 
     # roofline of the dominant kernel: the M2L product on the FP64 tensor cores
     # (DMMA.8x8x4): the frequency-space products of the FFT M2L, or the dense
@@ -290,13 +314,13 @@ def main():
     ng = 2 * spec.p - 1
     nf = ng * ng * (ng // 2 + 1)
     if mode == "fft":
-        m2l_flop = 8.0 * kml * kml * nf * info.n_v_pairs
+        m2l_flop = 8.0 * kml * kml * nf * n_v_local
         algo = (f"FFT M2L: 8 kml^2 flop per V pair per frequency bin, kml={kml}, NF={nf} (grid {ng}^3), "
-                f"{info.n_v_pairs} V pairs = {m2l_flop:.3e} flop")
+                f"{n_v_local} V pairs = {m2l_flop:.3e} flop")
         kname = "m2l product (k_m2l_dmma: per-frequency complex GEMM over parent blocks, DMMA.8x8x4)"
     else:
-        m2l_flop = 2.0 * n * n * info.n_v_pairs
-        algo = f"dense M2L: 2 n^2 flop per V pair, n={n}, {info.n_v_pairs} pairs = {m2l_flop:.3e} flop"
+        m2l_flop = 2.0 * n * n * n_v_local
+        algo = f"dense M2L: 2 n^2 flop per V pair, n={n}, {n_v_local} pairs = {m2l_flop:.3e} flop"
         kname = "m2l product (k_gemm_dmma: dense, grouped by V offset, DMMA.8x8x4)"
     peak_dmma = fp64_peak("dmma")
     peak_dfma = fp64_peak("dfma")
@@ -310,17 +334,19 @@ def main():
                 traffic = tj.get("m2l_dram_bytes_per_launch")
         except Exception:
             traffic = None
-    p2p_flop = P2P_FLOPS[spec.kernel] * info.n_p2p
+    p2p_flop = P2P_FLOPS[spec.kernel] * n_p2p_local
     stage_mean = {k: round(statistics.mean(s[k] for s in stages), 4) for k in stages[0]}
 
     line = {
         "metric": "FMM eval points/sec (N_S+N_T) at fixed p", "value": value, "unit": "points/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": workload_name(spec), "kernel": spec.kernel, "n": spec.n, "p": spec.p,
                    "max_pts_per_leaf": spec.cap, "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": f"{world} independent replicas" if world > 1 else "1 GPU",
+                   "parallelism": (f"{world} GPUs: one problem split into Morton ranges, NCCL exchanges "
+                                   "(values, shared + ghost multipoles, outputs); roofline/stages of rank 0")
+                   if world > 1 else "1 GPU",
                    "m2l": mode},
         "roofline": {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": peak_dmma,
                      "unit": "TFLOP/s", "frac": achieved / peak_dmma, "traffic": traffic,
@@ -329,7 +355,7 @@ def main():
                      "algorithmic": algo, "kernel_ms": prod_ms, "m2l_stage_ms": m2l_ms,
                      "m2l_stage_tflops": m2l_flop / (m2l_ms * 1e-3) / 1e12},
         "p2p": {"achieved_tflops": p2p_flop / (p2p_ms * 1e-3) / 1e12, "peak_dfma": peak_dfma,
-                "frac": p2p_flop / (p2p_ms * 1e-3) / 1e12 / peak_dfma, "pairs": info.n_p2p,
+                "frac": p2p_flop / (p2p_ms * 1e-3) / 1e12 / peak_dfma, "pairs": n_p2p_local,
                 "flop_per_pair": P2P_FLOPS[spec.kernel], "ms": p2p_ms},
         "stages_ms": stage_mean,
         "clocks": clocks,

@@ -37,6 +37,23 @@ static void free_plan(kafmm_plan_s* P) {
 
 using namespace kafmm;
 
+static void collect_stage_times(Plan& P) {
+  Plan* plan = &P;
+  if (plan->timing) {
+    KF_CUDA(cudaEventSynchronize(plan->ev[ST_TOTAL]));
+    for (int s = 0; s < ST_TOTAL; ++s) KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[s], plan->ev[s], plan->ev[s + 1]));
+    KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[ST_TOTAL], plan->ev[0], plan->ev[ST_TOTAL]));
+    float prod = 0.0f;
+    for (int i = 0; i + 1 < plan->prod_used; i += 2) {
+      float t = 0.0f;
+      KF_CUDA(cudaEventElapsedTime(&t, plan->prod_ev[i], plan->prod_ev[i + 1]));
+      prod += t;
+    }
+    plan->stage_ms[ST_M2L_PRODUCT] = prod;
+  }
+}
+
+
 #define KF_API_BEGIN try {
 #define KF_API_END                                 \
   }                                                \
@@ -141,18 +158,7 @@ kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_o
   }
   KF_API_BEGIN
   run_eval(*plan, src_values, trg_out);
-  if (plan->timing) {
-    KF_CUDA(cudaEventSynchronize(plan->ev[ST_TOTAL]));
-    for (int s = 0; s < ST_TOTAL; ++s) KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[s], plan->ev[s], plan->ev[s + 1]));
-    KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[ST_TOTAL], plan->ev[0], plan->ev[ST_TOTAL]));
-    float prod = 0.0f;
-    for (int i = 0; i + 1 < plan->prod_used; i += 2) {
-      float t = 0.0f;
-      KF_CUDA(cudaEventElapsedTime(&t, plan->prod_ev[i], plan->prod_ev[i + 1]));
-      prod += t;
-    }
-    plan->stage_ms[ST_M2L_PRODUCT] = prod;
-  }
+  collect_stage_times(*plan);
   return KAFMM_OK;
   KF_API_END
 }
@@ -362,6 +368,7 @@ kafmm_status kafmm_eval_down(kafmm_plan plan, double* trg_out) {
   }
   KF_API_BEGIN
   run_eval_down(*plan, trg_out);
+  collect_stage_times(*plan);
   return KAFMM_OK;
   KF_API_END
 }

@@ -344,7 +344,19 @@ def build_rank(global_points, caller_offsets, rank, world, kernel, p, cap, strea
     maps = rank_maps(T, cuts, np.asarray(caller_offsets, dtype=np.int64), rank)
     plan.restrict(maps.plo, maps.phi)
     n_local = int(caller_offsets[rank + 1] - caller_offsets[rank])
-    return RankPlan(plan, maps, n_local), cuts
+    rp = RankPlan(plan, maps, n_local)
+    rp.work = local_work(T, maps.plo, maps.phi)
+    return rp, cuts
+
+
+def local_work(T: GlobalTree, plo: int, phi: int) -> dict:
+    """V pairs and P2P pairs this rank's restricted plan evaluates."""
+    active = (T.pbeg < phi) & (T.pend > plo)
+    vt, _ = T.lists["V"]
+    ut, us = T.lists["U"]
+    npts = T.pend - T.pbeg
+    m = active[ut]
+    return {"n_v": int(active[vt].sum()), "n_p2p": int((npts[ut[m]] * npts[us[m]]).sum())}
 
 
 class DistKAFMM:
