@@ -154,9 +154,12 @@ kafmm_status kafmm_stage_times(kafmm_plan plan, float* ms /* KAFMM_N_STAGES */);
 const char* kafmm_stage_name(int stage);
 /* M2L variant used by kafmm_eval:
  *   0 = dense: raw kernel matrices grouped by V offset on the FP64 tensor cores
- *   1 = FFT (default when p is in {4,5,6,7,8,10,12}): convolution on the (2p)^3
- *       lattice grid, per-frequency products blocked by parent neighbourhoods.
- * Both compute the same matrices; results agree to rounding.  EINVAL for an
+ *   1 = FFT (default when p is in {3..8, 10, 12}): convolution on the (2p-1)^3
+ *       lattice grid; the frequency-space product runs per chunk of target
+ *       parents as DMMA parent blocks (8x8 child blocks x 26 directions), or
+ *       per V pair where fewer than 35% of those block entries are V pairs
+ *   2 = FFT, parent blocks everywhere;  3 = FFT, per V pair everywhere.
+ * All compute the same matrices; results agree to rounding.  EINVAL for an
  * unknown mode or FFT with an unsupported p.  (Environment KAFMM_M2L=dense at
  * setup selects dense.) */
 kafmm_status kafmm_set_m2l_mode(kafmm_plan plan, int mode);

@@ -327,8 +327,8 @@ const char* kafmm_stage_name(int s) {
 }
 
 kafmm_status kafmm_set_m2l_mode(kafmm_plan plan, int mode) {
-  if (!plan || (mode != 0 && mode != 1)) return KAFMM_EINVAL;
-  if (mode == 1 && plan->fft_chunks.empty() && plan->depth >= 2) {
+  if (!plan || mode < 0 || mode > 3) return KAFMM_EINVAL;
+  if (mode != 0 && plan->NF == 0 && plan->depth >= 2) {
     set_error("FFT M2L not available for this p");
     return KAFMM_EINVAL;
   }

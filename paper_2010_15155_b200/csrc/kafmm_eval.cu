@@ -368,7 +368,7 @@ static void eval_down_impl(Plan& P, double* d_out) {
   KF_CUDA(cudaMemsetAsync(P.d_chk, 0, (size_t)P.nbox * P.ldn * 8, st));
   mark(ST_M2L);
   P.prod_used = 0;
-  if (P.m2l_mode == M2L_FFT) {
+  if (P.m2l_mode != M2L_DENSE) {
     run_m2l_fft(P);
   } else {
     prod_mark(P);

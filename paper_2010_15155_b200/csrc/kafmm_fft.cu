@@ -99,6 +99,13 @@ __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
   acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
 }
 
+// The DFT passes below are direct sums over the p lattice points (or NG grid
+// frequencies) of one line.  Each thread produces FT outputs of one line from
+// a single read of every input value; the FT twiddles w^(f i) it needs at a
+// step are the same for every lane of the warp (lanes run over lines), so
+// their shared-memory reads are broadcasts.
+constexpr int FT = 5;
+
 // forward: one CTA per (source parent q, child octant c); the child's upward
 // equivalent density on the p^3 lattice (non-zero on the surface only) ->
 // its real DFT on the NG^3 grid, staged z (real -> half spectrum), y, x in
@@ -110,6 +117,7 @@ __global__ void __launch_bounds__(256)
               double2* __restrict__ ub) {
   using D = FftDims<P>;
   constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF;
+  constexpr int GZ = (NZ + FT - 1) / FT, GG = (NG + FT - 1) / FT;
   extern __shared__ __align__(16) double sm[];
   double* cube = sm;
   double2* A = reinterpret_cast<double2*>(sm + D::CUBE);  // [x][y][fz]
@@ -135,47 +143,83 @@ __global__ void __launch_bounds__(256)
     for (int m = tid; m < M; m += bd)
       cube[(lat[3 * m] * P + lat[3 * m + 1]) * P + lat[3 * m + 2]] = ue[box * ldn + m * kml + e];
     __syncthreads();
-    for (int idx = tid; idx < P * P * NZ; idx += bd) {  // z: real -> half spectrum
-      int xy = idx / NZ, fz = idx - xy * NZ;
+    for (int idx = tid; idx < GZ * P * P; idx += bd) {  // z: real -> half spectrum
+      const int g = idx / (P * P), xy = idx - g * P * P;
       const double* cc = cube + xy * P;
-      double re = 0.0, im = 0.0;
-      int k = 0;
+      double2 acc[FT];
+      int k[FT];
+#pragma unroll
+      for (int j = 0; j < FT; ++j) {
+        acc[j] = make_double2(0.0, 0.0);
+        k[j] = 0;
+      }
 #pragma unroll
       for (int z = 0; z < P; ++z) {
-        re = fma(cc[z], tw[k].x, re);
-        im = fma(cc[z], tw[k].y, im);
-        k += fz;
-        if (k >= NG) k -= NG;
+        const double v = cc[z];
+#pragma unroll
+        for (int j = 0; j < FT; ++j) {
+          const double2 w = tw[k[j]];
+          acc[j].x = fma(v, w.x, acc[j].x);
+          acc[j].y = fma(v, w.y, acc[j].y);
+          k[j] += g * FT + j;
+          if (k[j] >= NG) k[j] -= NG;
+        }
       }
-      A[idx] = make_double2(re, im);
+#pragma unroll
+      for (int j = 0; j < FT; ++j)
+        if (g * FT + j < NZ) A[xy * NZ + g * FT + j] = acc[j];
     }
     __syncthreads();
-    for (int idx = tid; idx < P * NG * NZ; idx += bd) {  // y
-      int x = idx / (NG * NZ), r = idx - x * NG * NZ, fy = r / NZ, fz = r - fy * NZ;
+    for (int idx = tid; idx < GG * P * NZ; idx += bd) {  // y
+      const int g = idx / (P * NZ), r = idx - g * P * NZ, x = r / NZ, fz = r - x * NZ;
       const double2* a = A + x * P * NZ + fz;
-      double2 acc = make_double2(0.0, 0.0);
-      int k = 0;
+      double2 acc[FT];
+      int k[FT];
+#pragma unroll
+      for (int j = 0; j < FT; ++j) {
+        acc[j] = make_double2(0.0, 0.0);
+        k[j] = 0;
+      }
 #pragma unroll
       for (int y = 0; y < P; ++y) {
-        cmac(acc, a[y * NZ], tw[k]);
-        k += fy;
-        if (k >= NG) k -= NG;
+        const double2 v = a[y * NZ];
+#pragma unroll
+        for (int j = 0; j < FT; ++j) {
+          cmac(acc[j], v, tw[k[j]]);
+          k[j] += g * FT + j;
+          if (k[j] >= NG) k[j] -= NG;
+        }
       }
-      B[idx] = acc;
+#pragma unroll
+      for (int j = 0; j < FT; ++j)
+        if (g * FT + j < NG) B[(x * NG + g * FT + j) * NZ + fz] = acc[j];
     }
     __syncthreads();
-    for (int idx = tid; idx < NF; idx += bd) {  // x
-      int fx = idx / (NG * NZ), r = idx - fx * NG * NZ;
+    for (int idx = tid; idx < GG * NG * NZ; idx += bd) {  // x
+      const int g = idx / (NG * NZ), r = idx - g * NG * NZ;
       const double2* bb = B + r;
-      double2 acc = make_double2(0.0, 0.0);
-      int k = 0;
+      double2 acc[FT];
+      int k[FT];
+#pragma unroll
+      for (int j = 0; j < FT; ++j) {
+        acc[j] = make_double2(0.0, 0.0);
+        k[j] = 0;
+      }
 #pragma unroll
       for (int x = 0; x < P; ++x) {
-        cmac(acc, bb[x * NG * NZ], tw[k]);
-        k += fx;
-        if (k >= NG) k -= NG;
+        const double2 v = bb[x * NG * NZ];
+#pragma unroll
+        for (int j = 0; j < FT; ++j) {
+          cmac(acc[j], v, tw[k[j]]);
+          k[j] += g * FT + j;
+          if (k[j] >= NG) k[j] -= NG;
+        }
       }
-      ub[((int64_t)idx * nq + q) * R + c * kml + e] = acc;
+#pragma unroll
+      for (int j = 0; j < FT; ++j) {
+        const int fx = g * FT + j;
+        if (fx < NG) ub[((int64_t)(fx * NG * NZ + r) * nq + q) * R + c * kml + e] = acc[j];
+      }
     }
     __syncthreads();
   }
@@ -191,6 +235,7 @@ __global__ void __launch_bounds__(256)
               const int16_t* __restrict__ lat, int M, double* __restrict__ chk, int ldn) {
   using D = FftDims<P>;
   constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF;
+  constexpr int GP = (P + FT - 1) / FT;
   extern __shared__ __align__(16) double sm[];
   double2* S = reinterpret_cast<double2*>(sm);  // [fx][fy][fz], then E [x][y][fz]
   double2* Dx = S + NF;                          // [x][fy][fz]
@@ -210,31 +255,53 @@ __global__ void __launch_bounds__(256)
     const double2* col = cb + (int64_t)pb.x * R + pb.y * kml + a;
     for (int f = tid; f < NF; f += bd) S[f] = col[(int64_t)f * npar * R];
     __syncthreads();
-    for (int idx = tid; idx < P * NG * NZ; idx += bd) {  // x: only x in [0, P)
-      int x = idx / (NG * NZ), r = idx - x * NG * NZ;
-      double2 acc = make_double2(0.0, 0.0);
-      int k = 0;
+    for (int idx = tid; idx < GP * NG * NZ; idx += bd) {  // x: only x in [0, P)
+      const int g = idx / (NG * NZ), r = idx - g * NG * NZ;
+      double2 acc[FT];
+      int k[FT];
+#pragma unroll
+      for (int j = 0; j < FT; ++j) {
+        acc[j] = make_double2(0.0, 0.0);
+        k[j] = 0;
+      }
 #pragma unroll 4
       for (int fx = 0; fx < NG; ++fx) {
-        cmac(acc, S[fx * NG * NZ + r], tw[k]);
-        k += x;
-        if (k >= NG) k -= NG;
+        const double2 v = S[fx * NG * NZ + r];
+#pragma unroll
+        for (int j = 0; j < FT; ++j) {
+          cmac(acc[j], v, tw[k[j]]);
+          k[j] += g * FT + j;
+          if (k[j] >= NG) k[j] -= NG;
+        }
       }
-      Dx[idx] = acc;
+#pragma unroll
+      for (int j = 0; j < FT; ++j)
+        if (g * FT + j < P) Dx[(g * FT + j) * NG * NZ + r] = acc[j];
     }
     __syncthreads();
-    for (int idx = tid; idx < P * P * NZ; idx += bd) {  // y: only y in [0, P)
-      int x = idx / (P * NZ), r = idx - x * P * NZ, y = r / NZ, fz = r - y * NZ;
+    for (int idx = tid; idx < GP * P * NZ; idx += bd) {  // y: only y in [0, P)
+      const int g = idx / (P * NZ), r = idx - g * P * NZ, x = r / NZ, fz = r - x * NZ;
       const double2* d = Dx + x * NG * NZ + fz;
-      double2 acc = make_double2(0.0, 0.0);
-      int k = 0;
+      double2 acc[FT];
+      int k[FT];
+#pragma unroll
+      for (int j = 0; j < FT; ++j) {
+        acc[j] = make_double2(0.0, 0.0);
+        k[j] = 0;
+      }
 #pragma unroll 4
       for (int fy = 0; fy < NG; ++fy) {
-        cmac(acc, d[fy * NZ], tw[k]);
-        k += y;
-        if (k >= NG) k -= NG;
+        const double2 v = d[fy * NZ];
+#pragma unroll
+        for (int j = 0; j < FT; ++j) {
+          cmac(acc[j], v, tw[k[j]]);
+          k[j] += g * FT + j;
+          if (k[j] >= NG) k[j] -= NG;
+        }
       }
-      E[idx] = acc;
+#pragma unroll
+      for (int j = 0; j < FT; ++j)
+        if (g * FT + j < P) E[(x * P + g * FT + j) * NZ + fz] = acc[j];
     }
     __syncthreads();
     double* o = chk + box * ldn;
@@ -292,13 +359,19 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[m][n][0][0] = acc[m][n][0][1] = acc[m][n][1][0] = acc[m][n][1][1] = 0.0;
   const double2* ubf = ub + f * nq * R;
+  int qn[NT];  // colleague block of the next direction (prefetched)
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const int64_t Pn = P0 + n * 8 + g;
+    qn[n] = Pn < npar ? nbr[Pn * 26] : -1;
+  }
   for (int d = 0; d < 26; ++d) {
     int64_t qb[NT];
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
+      qb[n] = qn[n] >= 0 ? (int64_t)qn[n] * R + tq : -1;
       const int64_t Pn = P0 + n * 8 + g;
-      const int qq = Pn < npar ? nbr[Pn * 26 + d] : -1;
-      qb[n] = qq >= 0 ? (int64_t)qq * R + tq : -1;
+      qn[n] = (d + 1 < 26 && Pn < npar) ? nbr[Pn * 26 + d + 1] : -1;
     }
     {  // a direction none of the warp's parents has a (non-leaf) colleague in: no work
       bool any = false;
@@ -341,6 +414,56 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
         const int64_t Pn = P0 + n * 8 + 2 * tq + e;
         if (Pn < npar) cbf[Pn * R + m * 8 + g] = make_double2(acc[m][n][0][e], acc[m][n][1][e]);
       }
+}
+
+// The same product per V pair, for chunks whose parent blocks are mostly
+// empty (sparse adaptive trees): one thread per (target box, frequency), the
+// frequency's operator spectra in shared memory, the target's V list walked
+// with the source spectra read from ub and the sum kept in registers.
+constexpr int PAIR_THREADS = 128;
+
+template <int KML>
+__global__ void __launch_bounds__(PAIR_THREADS)
+    k_m2l_pairs(int64_t nt, int64_t nq, int64_t npar, int ntb, const double2* __restrict__ that,
+                const double2* __restrict__ ub, double2* __restrict__ cb, const int2* __restrict__ tpb,
+                const int64_t* __restrict__ off, const int32_t* __restrict__ pl) {
+  constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
+  __shared__ double2 sT[N_OFFSETS * NC];
+  const int64_t f = blockIdx.x / ntb;
+  const int tb = blockIdx.x % ntb;
+  for (int i = threadIdx.x; i < N_OFFSETS * NC; i += PAIR_THREADS) sT[i] = that[f * N_OFFSETS * NC + i];
+  __syncthreads();
+  const int64_t t = (int64_t)tb * PAIR_THREADS + threadIdx.x;
+  if (t >= nt) return;
+  const double2* ubf = ub + f * nq * R;
+  double2 acc[KML];
+#pragma unroll
+  for (int a = 0; a < KML; ++a) acc[a] = make_double2(0.0, 0.0);
+  const int64_t e1 = off[t + 1];
+  for (int64_t e = off[t]; e < e1; ++e) {
+    const int v = pl[e];
+    const double2* u = ubf + (int64_t)(v >> 9) * KML;
+    const double2* T = sT + (v & 511) * NC;
+    if (KML == 1) {
+      cmac(acc[0], T[0], u[0]);
+    } else {
+      const double2 u0 = u[0], u1 = u[1], u2 = u[2];
+      const double2 t0 = T[0], t1 = T[1], t2 = T[2], t3 = T[3], t4 = T[4], t5 = T[5];
+      cmac(acc[0], t0, u0);
+      cmac(acc[0], t1, u1);
+      cmac(acc[0], t2, u2);
+      cmac(acc[KML > 1 ? 1 : 0], t1, u0);
+      cmac(acc[KML > 1 ? 1 : 0], t3, u1);
+      cmac(acc[KML > 1 ? 1 : 0], t4, u2);
+      cmac(acc[KML > 2 ? 2 : 0], t2, u0);
+      cmac(acc[KML > 2 ? 2 : 0], t4, u1);
+      cmac(acc[KML > 2 ? 2 : 0], t5, u2);
+    }
+  }
+  const int2 pb = tpb[t];
+  double2* o = cb + (f * npar + pb.x) * R + pb.y * KML;
+#pragma unroll
+  for (int a = 0; a < KML; ++a) o[a] = acc[a];
 }
 
 // ---------------------------------------------------------------------------
@@ -395,16 +518,28 @@ void run_m2l_fft(Plan& Pl) {
   for (const FftChunk& ch : Pl.fft_chunks) {
     if (ch.nt == 0 || ch.nq == 0) continue;
     KF_FFT_DISPATCH(launch_fwd);
-    const int ppc = DM_WARPS * 8 * (Pl.kml == 1 ? NT_L : NT_G);
-    const int npb = (int)((ch.npar + ppc - 1) / ppc);
-    const unsigned grid = (unsigned)((int64_t)npb * Pl.NF);
+    const bool pairs = Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < FFT_PAIR_FILL);
     prod_mark(Pl);
-    if (Pl.kml == 1)
-      k_m2l_dmma<1, NT_L><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb,
-                                                                 ch.d_nbr, Pl.d_aidx);
-    else
-      k_m2l_dmma<3, NT_G><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb,
-                                                                 ch.d_nbr, Pl.d_aidx);
+    if (pairs) {
+      const int ntb = (int)((ch.nt + PAIR_THREADS - 1) / PAIR_THREADS);
+      const unsigned grid = (unsigned)((int64_t)ntb * Pl.NF);
+      if (Pl.kml == 1)
+        k_m2l_pairs<1><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
+                                                             Pl.d_cb, ch.d_tpb, ch.d_pl_off, ch.d_pl);
+      else
+        k_m2l_pairs<3><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
+                                                             Pl.d_cb, ch.d_tpb, ch.d_pl_off, ch.d_pl);
+    } else {
+      const int ppc = DM_WARPS * 8 * (Pl.kml == 1 ? NT_L : NT_G);
+      const int npb = (int)((ch.npar + ppc - 1) / ppc);
+      const unsigned grid = (unsigned)((int64_t)npb * Pl.NF);
+      if (Pl.kml == 1)
+        k_m2l_dmma<1, NT_L><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb,
+                                                                   ch.d_nbr, Pl.d_aidx);
+      else
+        k_m2l_dmma<3, NT_G><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb,
+                                                                   ch.d_nbr, Pl.d_aidx);
+    }
     KF_CHECK_LAUNCH();
     prod_mark(Pl);
     Pl.launches++;
@@ -538,6 +673,27 @@ void build_fft_chunks(Plan& P, int64_t budget) {
     auto it = std::lower_bound(b, e, kk);
     return (it != e && *it == kk) ? (int64_t)(it - key.begin()) : -1;
   };
+  // V lists by target box (from the (src, tgt) pairs sorted by level/offset)
+  std::vector<int2> vp;
+  d2h(P, vp, P.d_v_pairs, P.n_v);
+  std::vector<int64_t> voff(P.nbox + 1, 0);
+  for (const int2& q : vp) voff[q.y + 1]++;
+  for (int64_t b = 0; b < P.nbox; ++b) voff[b + 1] += voff[b];
+  std::vector<int32_t> vsrc(P.n_v);
+  {
+    std::vector<int64_t> fill(voff.begin(), voff.end() - 1);
+    for (const int2& q : vp) vsrc[fill[q.y]++] = q.x;
+  }
+  std::vector<int32_t> parent;
+  d2h(P, parent, P.d_parent, P.nbox);
+  int16_t offid[343];
+  {
+    int id = 0;
+    for (int a = 0; a < 343; ++a) {
+      int ox = a / 49 - 3, oy = (a / 7) % 7 - 3, oz = a % 7 - 3;
+      offid[a] = (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) >= 2) ? (int16_t)id++ : (int16_t)-1;
+    }
+  }
   const int64_t per_block = (int64_t)R * P.NF * 16;  // one parent block of spectra
   P.fft_chunks.clear();
   P.fft_max_nq = P.fft_max_npar = 0;
@@ -588,6 +744,32 @@ void build_fft_chunks(Plan& P, int64_t budget) {
           }
         }
       ch.nt = (int64_t)tb.size();
+      std::vector<int64_t> ploff(1, 0);
+      std::vector<int32_t> pl;
+      for (int32_t t : tb) {
+        for (int64_t e = voff[t]; e < voff[t + 1]; ++e) {
+          const int32_t sb = vsrc[e];
+          const int32_t q = qlocal[parent[sb]];
+          const int c = 4 * (ijk[3 * sb] & 1) + 2 * (ijk[3 * sb + 1] & 1) + (ijk[3 * sb + 2] & 1);
+          const int ox = ijk[3 * sb] - ijk[3 * t], oy = ijk[3 * sb + 1] - ijk[3 * t + 1],
+                    oz = ijk[3 * sb + 2] - ijk[3 * t + 2];
+          const int oid = offid[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)];
+          if (q < 0 || oid < 0) throw Error{KAFMM_ECUDA, "FFT M2L: V source outside the chunk's parent blocks"};
+          pl.push_back((int32_t)((q * 8 + c) << 9 | oid));
+        }
+        ploff.push_back((int64_t)pl.size());
+      }
+      if ((int64_t)qs.size() * 8 >= (1 << 22)) throw Error{KAFMM_EINVAL, "FFT M2L chunk too large for pair indices"};
+      ch.npairs = (int64_t)pl.size();
+      {
+        int64_t blocks = 0;
+        for (int32_t v : nb) blocks += v >= 0;
+        ch.block_fill = blocks ? (double)ch.npairs / (64.0 * (double)blocks) : 1.0;
+      }
+      ch.d_pl_off = dalloc<int64_t>(P, ploff.size());
+      ch.d_pl = dalloc<int32_t>(P, std::max<size_t>(1, pl.size()));
+      KF_CUDA(cudaMemcpyAsync(ch.d_pl_off, ploff.data(), ploff.size() * 8, cudaMemcpyHostToDevice, st));
+      if (!pl.empty()) KF_CUDA(cudaMemcpyAsync(ch.d_pl, pl.data(), pl.size() * 4, cudaMemcpyHostToDevice, st));
       ch.d_qbox = dalloc<int32_t>(P, std::max<int64_t>(1, ch.nq));
       ch.d_nbr = dalloc<int32_t>(P, ch.npar * 26);
       ch.d_tbox = dalloc<int32_t>(P, std::max<int64_t>(1, ch.nt));

@@ -58,9 +58,19 @@ struct FftChunk {
   int32_t* d_nbr = nullptr;   // npar x 26: local q of the colleague in direction d, or -1
   int32_t* d_tbox = nullptr;  // nt target box ids
   int2* d_tpb = nullptr;      // nt: (local parent index, child octant)
+  // the same V pairs as a per-target list (for sparse chunks): entry
+  // (q * 8 + c) << 9 | offset id, source = child c of source parent q
+  int64_t npairs = 0;
+  int64_t* d_pl_off = nullptr;  // nt + 1
+  int32_t* d_pl = nullptr;      // npairs
+  double block_fill = 1.0;      // V pairs / (8x8 child blocks the DMMA product runs)
 };
 
-enum M2LMode { M2L_DENSE = 0, M2L_FFT = 1 };
+// M2L variants: dense per-offset GEMMs, or the FFT lattice convolution whose
+// frequency-space product runs per chunk as DMMA parent blocks or, where the
+// blocks are mostly empty (sparse adaptive trees), per V pair.
+enum M2LMode { M2L_DENSE = 0, M2L_FFT = 1, M2L_FFT_BLOCKS = 2, M2L_FFT_PAIRS = 3 };
+constexpr double FFT_PAIR_FILL = 0.35;  // block fill below which a chunk runs per pair (M2L_FFT)
 
 // The work lists the evaluation kernels run over.  For a plan built by
 // kafmm_setup they alias the full lists; kafmm_restrict (multi-GPU, one rank

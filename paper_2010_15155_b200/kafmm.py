@@ -222,14 +222,17 @@ class KAFMM:
         _check(self.lib.kafmm_stage_times(self.h, arr), "kafmm_stage_times")
         return {self.lib.kafmm_stage_name(i).decode(): float(arr[i]) for i in range(N_STAGES)}
 
+    M2L_MODES = {"dense": 0, "fft": 1, "fft_blocks": 2, "fft_pairs": 3}
+
     def set_m2l(self, mode: str):
-        """'dense' (FP64 tensor-core GEMMs) or 'fft' (lattice convolution)."""
-        _check(self.lib.kafmm_set_m2l_mode(self.h, {"dense": 0, "fft": 1}[mode]), "kafmm_set_m2l_mode")
+        """'dense' (FP64 tensor-core GEMMs), 'fft' (lattice convolution, product
+        per chunk by block fill), 'fft_blocks' or 'fft_pairs' (forced product)."""
+        _check(self.lib.kafmm_set_m2l_mode(self.h, self.M2L_MODES[mode]), "kafmm_set_m2l_mode")
 
     def m2l(self) -> str:
         m = C.c_int()
         _check(self.lib.kafmm_get_m2l_mode(self.h, C.byref(m)), "kafmm_get_m2l_mode")
-        return ["dense", "fft"][m.value]
+        return ["dense", "fft", "fft_blocks", "fft_pairs"][m.value]
 
     # multi-GPU building blocks (dist.py)
     def restrict(self, plo: int, phi: int):

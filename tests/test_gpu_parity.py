@@ -36,14 +36,21 @@ CASES = [
     ("rpy_uniform", "rpy", lambda: np.random.default_rng(5).random((3000, 3)), 6, 40),
     ("regvel_clustered", "stokes_reg_vel", lambda: _clustered(4000, 6), 6, 32),
     ("stokeslet_spheres", "stokeslet", lambda: WL.make_points(WL.CONFIGS[5], 12000, n_spheres=60), 6, 64),
+    # polydisperse b / eps on the paper's log-normal cloud (C6, C7 shapes)
+    ("C6_poly_rpy", "rpy", lambda: WL.make_points(WL.CONFIGS[6], 12000), 8, 150),
+    ("C7_poly_regvel", "stokes_reg_vel", lambda: WL.make_points(WL.CONFIGS[7], 12000), 8, 150),
 ]
+POLY = {"C6_poly_rpy": 6, "C7_poly_regvel": 7}
 
 
 @pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
 def case(request):
     name, kernel, mk, p, cap = request.param
     pts = mk()
-    vals = WL.random_values(kernel, pts.shape[0], 17)
+    if name in POLY:
+        vals = WL.make_values(WL.CONFIGS[POLY[name]], pts.shape[0])
+    else:
+        vals = WL.random_values(kernel, pts.shape[0], 17)
     plan, gpu = run_gpu(pts, vals, kernel, p, cap)
     ref = F.fmm(pts, vals, kernel, p, cap, keep_internals=True)
     return dict(name=name, kernel=kernel, pts=pts, vals=vals, p=p, cap=cap, plan=plan, gpu=gpu, ref=ref)

@@ -123,3 +123,20 @@ def test_sampled_mode_equals_full(kernel):
     leaves = F.sample_leaves(t, 150, seed=4)
     s = F.fmm(pts, vals, kernel, 5, 25, target_leaves=leaves, tree=t)
     np.testing.assert_allclose(s["out"], full["out"][s["idx"]], rtol=0, atol=1e-13 * np.abs(s["out"]).max())
+
+
+@pytest.mark.parametrize("cid", [6, 7])
+def test_polydisperse_lognormal_error_decreases_with_p(cid):
+    # SURVEY.md §8(f) rank 1 / PAPER.md:674-679: polydisperse b (RPY) and eps
+    # (RegVel) iid U[0, 1e-4] on the Eq. (ptdist) cloud; "exponentially
+    # decreasing convergence error" -- here against the O1 direct sum, per block
+    import workloads as WL
+    spec, pts, vals = WL.make_config(cid, n=1500)
+    assert vals[:, 3].min() >= 0.0 and vals[:, 3].max() <= spec.extra and np.ptp(vals[:, 3]) > 0
+    d = F.direct(spec.kernel, pts, vals)
+    errs = []
+    for p in (4, 6, 8):
+        out = F.fmm(pts, vals, spec.kernel, p, 60)["out"]
+        errs.append(max(F.rel_l2(out[:, lo:hi], d[:, lo:hi]) for lo, hi in F.blocks(spec.kernel)))
+    for e0, e1 in zip(errs, errs[1:]):
+        assert e1 < e0 / 10.0, errs

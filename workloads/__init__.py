@@ -18,6 +18,13 @@ Recipe:
   C5      10^4 sphere centres by random sequential addition in [r, 1-r]^3,
           r = 0.005, centre distance >= 2r; 6,400 points per sphere
           y = c + r v/|v|, v ~ N(0, I); Stokeslet, p=8, cap 128
+  C6, C7 (not BASELINE configs) the paper's own
+          benchmark cloud, Eq. (ptdist): x, y, z iid
+          u - [u] with u log-normal (m = -1, s = 0.5), i.e. the paper's
+          L (u - [u]) with L = 32 scaled to the unit cube; N = 10^6, leaf cap
+          2000, values U[-1, 1], polydisperse
+          b (C6, RPY) or eps (C7, RegVel) iid U[0, 1e-4] in the paper's units
+          (PAPER.md:676), i.e. U[0, 1e-4 / 32] in the unit cube; p = 10
 The BASELINE configs are the paper-shaped stand-ins for the paper's own
 synthetic clouds (Eq. (ptdist)); no dataset is involved.
 """
@@ -42,8 +49,9 @@ class ConfigSpec:
     n: int
     p: int
     cap: int
-    cloud: str          # "uniform" | "clusters" | "spheres"
+    cloud: str          # "uniform" | "clusters" | "spheres" | "lognormal"
     extra: float = 0.0  # b (RPY) or eps (RegVel) carried as the 4th source column
+    poly: bool = False  # 4th column iid U[0, extra] per source; values U[-1, 1] (paper's benchmarks)
 
     @property
     def name(self) -> str:
@@ -56,7 +64,10 @@ CONFIGS = {
     3: ConfigSpec(3, "rpy", 4_000_000, 10, 64, "uniform", 1e-3),
     4: ConfigSpec(4, "stokes_reg_vel", 8_000_000, 12, 64, "clusters", 1e-4),
     5: ConfigSpec(5, "stokeslet", 64_000_000, 8, 128, "spheres"),
+    6: ConfigSpec(6, "rpy", 1_000_000, 10, 2000, "lognormal", 1e-4 / 32, True),
+    7: ConfigSpec(7, "stokes_reg_vel", 1_000_000, 10, 2000, "lognormal", 1e-4 / 32, True),
 }
+LOGNORMAL_M, LOGNORMAL_S = -1.0, 0.5
 
 
 def _streams(cid: int):
@@ -138,6 +149,9 @@ def make_points(spec: ConfigSpec, n: int | None = None, n_spheres: int | None = 
     elif spec.cloud == "spheres":
         ns = 10_000 if n_spheres is None else int(n_spheres)
         pts = _spheres(rp, rc, n, n_spheres=min(ns, max(1, n)))
+    elif spec.cloud == "lognormal":
+        u = rp.lognormal(LOGNORMAL_M, LOGNORMAL_S, size=(n, 3))
+        pts = u - np.floor(u)
     else:
         raise ValueError(spec.cloud)
     assert np.all((pts >= 0.0) & (pts < 1.0))
@@ -148,7 +162,10 @@ def make_values(spec: ConfigSpec, n: int | None = None):
     n = spec.n if n is None else int(n)
     _rp, rv, _rc = _streams(spec.cid)
     k_s = KERNEL_DIMS[spec.kernel][0]
-    if spec.kernel == "laplace_pgrad":
+    if spec.poly:
+        vals = rv.uniform(-1.0, 1.0, size=(n, k_s))
+        vals[:, 3] = rv.uniform(0.0, spec.extra, size=n)
+    elif spec.kernel == "laplace_pgrad":
         vals = rv.standard_normal((n, 1))
     elif spec.kernel == "stokeslet":
         vals = rv.standard_normal((n, 3))
