@@ -54,13 +54,17 @@ typedef enum {
  *                   (Eqs. RPYflow/RPYkernel, Table IV); the target
  *                   radius assembly u + a^2/6 lap u (Eq. RPYtrgvel) is the caller's
  *   STOKES_REG_VEL  k_s=4 [f, eps]   k_t=3 [u], u = sum G^eps f
- * Self pairs (r^2 == 0) are skipped by the singular kernels and kept by
- * STOKES_REG_VEL, where G^eps(0) = 1/(4 pi eps) is finite. */
+ *   STOKES_REG_VEL_OMEGA  k_s=7 [f, t, eps]  k_t=6 [u, omega]:
+ *                   u = sum G^eps f + T^eps t, omega = sum Omega^eps f + W^eps t
+ *                   (Table VI; ML tree G, T column G (+) Omega)
+ * Self pairs (r^2 == 0) are skipped by the singular kernels and kept by the
+ * regularized ones, where G^eps(0) = 1/(4 pi eps) is finite. */
 typedef enum {
   KAFMM_LAPLACE_PGRAD = 1,
   KAFMM_STOKESLET = 2,
   KAFMM_RPY = 3,
-  KAFMM_STOKES_REG_VEL = 4
+  KAFMM_STOKES_REG_VEL = 4,
+  KAFMM_STOKES_REG_VEL_OMEGA = 5
 } kafmm_kernel;
 
 /* Source and target dimensions of a kernel.  EINVAL for an unknown kernel. */

@@ -8,6 +8,8 @@ Kernel tables (which kernel each of the 8 traversal stages uses):
   RPY       Table IV: S-row G_RPY, ML tree G,
             T column G+lapG, S2T G_RPY+lapG
   RegVel    Table V: S-row G_eps, ML tree and T column G
+  RegVelOmega Table VI: S-row G_eps+T_eps, ML tree G,
+            T column G+Omega, S2T G_eps+Omega+T+W
 
 Steps, in the paper's order (Fig. 1):
   S->M   leaf sources -> upward check surface -> UC2UE (two SVD factors)
@@ -38,6 +40,8 @@ TABLES = {
     "stokeslet": dict(S="G", ML="G", T="G", ST="G"),
     "rpy": dict(S="G_RPY", ML="G", T="G+lapG", ST="G_RPY+lapG"),
     "stokes_reg_vel": dict(S="G_eps", ML="G", T="G", ST="G_eps"),
+    # Table VI: [f, t, eps] -> [u, omega]
+    "stokes_reg_vel_omega": dict(S="G_eps+T_eps", ML="G", T="G+Omega", ST="G_eps+Omega+T+W"),
 }
 
 _OPS_CACHE: dict = {}
@@ -232,4 +236,5 @@ def rel_l2(a, b) -> float:
 def blocks(kernel: str):
     """Output blocks per reading R11 (phi | grad phi ; u | lap u)."""
     return {"laplace_pgrad": [(0, 1), (1, 4)], "stokeslet": [(0, 3)],
-            "rpy": [(0, 3), (3, 6)], "stokes_reg_vel": [(0, 3)]}[kernel]
+            "rpy": [(0, 3), (3, 6)], "stokes_reg_vel": [(0, 3)],
+            "stokes_reg_vel_omega": [(0, 3), (3, 6)]}[kernel]

@@ -12,6 +12,12 @@ Kernel names follow the paper's notation:
   G_RPY+lapG [u, lap u]; lap G^RPY = lap G since lap lap G = 0
   G+lapG     [u, lap u] from point forces                          PAPER.md:106, Table IV
   G_eps      regularized Stokeslet
+  G_eps+T_eps            [f, t, eps] -> u = G^eps f + T^eps t        Table VI S-row, PAPER.md:357-362
+  G+Omega                f -> [u, omega] = [G f, Omega f] (eps = 0)  Table VI T column
+  G_eps+Omega+T+W        [f, t, eps] -> [u, omega], the 7x6 S->T     PAPER.md:356-374, Table VI
+with H1, H2, Q, D1, D2 of PAPER.md:363-369 (1/(8 pi) inside) and
+Omega^eps_ij = T^eps_ij = Q eps_ijk r_k / 2, so Omega f = Q (f x r) / 2 and
+T t = Q (t x r) / 2; W^eps = D1 delta / 4 + D2 r r^T / 4.
 with lap G_ij = (1/8pi)(2 delta_ij / r^3 - 6 r_i r_j / r^5) (derived from
 G_ij; checked by finite differences in tests/test_oracle_kernels.py).
 
@@ -34,9 +40,13 @@ DIMS = {
     "G_RPY+lapG": (4, 6),
     "G+lapG": (3, 6),
     "G_eps": (4, 3),
+    "G_eps+T_eps": (7, 3),
+    "G+Omega": (3, 6),
+    "G_eps+Omega+T+W": (7, 6),
 }
 SINGULAR = {"L": True, "L+gradL": True, "G": True, "G_RPY": True, "G_RPY+lapG": True,
-            "G+lapG": True, "G_eps": False}
+            "G+lapG": True, "G_eps": False, "G_eps+T_eps": False, "G+Omega": True,
+            "G_eps+Omega+T+W": False}
 
 
 def pair_values(name: str, r: np.ndarray, s: np.ndarray) -> np.ndarray:
@@ -46,6 +56,26 @@ def pair_values(name: str, r: np.ndarray, s: np.ndarray) -> np.ndarray:
     r^2 == 0 contribute zero for singular kernels.
     """
     r2 = np.sum(r * r, axis=-1)
+    if name in ("G_eps+T_eps", "G_eps+Omega+T+W"):
+        f, t, eps = s[..., 0:3], s[..., 3:6], s[..., 6]
+        e2 = eps * eps
+        d = e2 + r2
+        sd = np.sqrt(d)
+        d32 = d * sd
+        d52 = d32 * d
+        d72 = d52 * d
+        H1 = (2.0 * e2 + r2) / (EIGHT_PI * d32)                          # PAPER.md:363
+        H2 = 1.0 / (EIGHT_PI * d32)                                      # PAPER.md:364
+        Q = (5.0 * e2 + 2.0 * r2) / (EIGHT_PI * d52)                     # PAPER.md:365
+        rf = np.sum(r * f, axis=-1)
+        u = H1[..., None] * f + (H2 * rf)[..., None] * r + 0.5 * Q[..., None] * np.cross(t, r)
+        if name == "G_eps+T_eps":
+            return u
+        D1 = (10.0 * e2 * e2 - 7.0 * e2 * r2 - 2.0 * r2 * r2) / (EIGHT_PI * d72)  # PAPER.md:366
+        D2 = (21.0 * e2 + 6.0 * r2) / (EIGHT_PI * d72)                            # PAPER.md:367
+        rt = np.sum(r * t, axis=-1)
+        w = 0.5 * Q[..., None] * np.cross(f, r) + 0.25 * D1[..., None] * t + (0.25 * D2 * rt)[..., None] * r
+        return np.concatenate([u, w], axis=-1)
     if name == "G_eps":
         eps = s[..., 3]
         f = s[..., :3]
@@ -70,6 +100,10 @@ def pair_values(name: str, r: np.ndarray, s: np.ndarray) -> np.ndarray:
     rf = np.sum(r * f, axis=-1)
     if name == "G":
         return (rinv[..., None] * f + (rf * rinv3)[..., None] * r) / EIGHT_PI
+    if name == "G+Omega":  # Q(r) at eps = 0 is 2 / (8 pi r^3)
+        u = (rinv[..., None] * f + (rf * rinv3)[..., None] * r) / EIGHT_PI
+        w = rinv3[..., None] * np.cross(f, r) / EIGHT_PI
+        return np.concatenate([u, w], axis=-1)
     rinv5 = rinv3 * rinv * rinv
     lap = (2.0 * rinv3[..., None] * f - 6.0 * (rf * rinv5)[..., None] * r) / EIGHT_PI
     if name == "G+lapG":

@@ -19,6 +19,7 @@ static int dims(int kernel, int* ks, int* kt) {
     case KAFMM_STOKESLET: *ks = 3; *kt = 3; return 0;
     case KAFMM_RPY: *ks = 4; *kt = 6; return 0;
     case KAFMM_STOKES_REG_VEL: *ks = 4; *kt = 3; return 0;
+    case KAFMM_STOKES_REG_VEL_OMEGA: *ks = 7; *kt = 6; return 0;
     default: return -1;
   }
 }
@@ -103,7 +104,7 @@ kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int
   P->ks = ks;
   P->kt = kt;
   P->kml = (kernel == KAFMM_LAPLACE_PGRAD) ? 1 : 3;
-  P->srec = (kernel == KAFMM_LAPLACE_PGRAD) ? 4 : 8;
+  P->srec = (kernel == KAFMM_LAPLACE_PGRAD) ? 4 : (kernel == KAFMM_STOKES_REG_VEL_OMEGA ? 12 : 8);
   P->M = 6 * (p - 1) * (p - 1) + 2;
   P->neq = P->kml * P->M;
   P->ldn = round_up(P->neq, GEMM_BK);

@@ -38,20 +38,17 @@ __global__ void k_gather(const double* __restrict__ vals, const double* __restri
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t u = perm[i];
-  double r[8];
+  double r[12];
   r[0] = pts[4 * i];
   r[1] = pts[4 * i + 1];
   r[2] = pts[4 * i + 2];
 #pragma unroll
-  for (int c = 3; c < 8; ++c) r[c] = 0.0;
+  for (int c = 3; c < 12; ++c) r[c] = 0.0;
   for (int c = 0; c < ks; ++c) r[3 + c] = vals[u * ks + c];
-  if (srec == 4) {
-    reinterpret_cast<double2*>(rec + 4 * i)[0] = make_double2(r[0], r[1]);
-    reinterpret_cast<double2*>(rec + 4 * i)[1] = make_double2(r[2], r[3]);
-  } else {
+  double2* o = reinterpret_cast<double2*>(rec + (int64_t)srec * i);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) reinterpret_cast<double2*>(rec + 8 * i)[c] = make_double2(r[2 * c], r[2 * c + 1]);
-  }
+  for (int c = 0; c < 6; ++c)
+    if (2 * c < srec) o[c] = make_double2(r[2 * c], r[2 * c + 1]);
 }
 
 // Source streaming shared by the pointwise kernels: the CTA walks a list of
@@ -198,16 +195,25 @@ __global__ void __launch_bounds__(PT_THREADS)
     const bool act = z.sl < z.S;
     const int64_t ti = t0 + z.tt;
     const double tx = pts[4 * ti], ty = pts[4 * ti + 1], tz = pts[4 * ti + 2];
-    double acc[K::KT];
+    double acc[K::KT], acc2[K::KT];
 #pragma unroll
-    for (int a = 0; a < K::KT; ++a) acc[a] = 0.0;
+    for (int a = 0; a < K::KT; ++a) acc[a] = acc2[a] = 0.0;
     auto run = [&](int cnt) {
       __syncthreads();
-      if (act)
-        for (int j = z.sl; j < cnt; j += z.S) {
+      if (act) {
+        // two interleaved accumulator sets: independent dependency chains (ILP)
+        int j = z.sl;
+        for (; j + z.S < cnt; j += 2 * z.S) {
+          const double* sr = ss + j * SSTR;
+          const double* s2 = sr + z.S * SSTR;
+          K::acc(tx - sr[0], ty - sr[1], tz - sr[2], sr + 3, acc);
+          K::acc(tx - s2[0], ty - s2[1], tz - s2[2], s2 + 3, acc2);
+        }
+        if (j < cnt) {
           const double* sr = ss + j * SSTR;
           K::acc(tx - sr[0], ty - sr[1], tz - sr[2], sr + 3, acc);
         }
+      }
       __syncthreads();
     };
     int fill = 0;
@@ -238,6 +244,8 @@ __global__ void __launch_bounds__(PT_THREADS)
       }
     }
     if (fill) run(fill);
+#pragma unroll
+    for (int a = 0; a < K::KT; ++a) acc[a] += acc2[a];
     slice_reduce_store<K::KT>(z, acc, red, outs + t0 * K::KT, false);
   }
 }
@@ -260,16 +268,25 @@ __global__ void __launch_bounds__(PT_THREADS)
     const bool act = z.sl < z.S;
     const int64_t ti = t0 + z.tt;
     const double tx = rec[SREC * ti], ty = rec[SREC * ti + 1], tz = rec[SREC * ti + 2];
-    double acc[K::KT];
+    double acc[K::KT], acc2[K::KT];
 #pragma unroll
-    for (int a = 0; a < K::KT; ++a) acc[a] = 0.0;
+    for (int a = 0; a < K::KT; ++a) acc[a] = acc2[a] = 0.0;
     auto run = [&](int cnt) {
       __syncthreads();
-      if (act)
-        for (int j = z.sl; j < cnt; j += z.S) {
+      if (act) {
+        // two interleaved accumulator sets: independent dependency chains (ILP)
+        int j = z.sl;
+        for (; j + z.S < cnt; j += 2 * z.S) {
+          const double* sr = ss + j * SREC;
+          const double* s2 = sr + z.S * SREC;
+          K::acc(tx - sr[0], ty - sr[1], tz - sr[2], sr + 3, acc);
+          K::acc(tx - s2[0], ty - s2[1], tz - s2[2], s2 + 3, acc2);
+        }
+        if (j < cnt) {
           const double* sr = ss + j * SREC;
           K::acc(tx - sr[0], ty - sr[1], tz - sr[2], sr + 3, acc);
         }
+      }
       __syncthreads();
     };
     int fill = 0;
@@ -289,6 +306,8 @@ __global__ void __launch_bounds__(PT_THREADS)
       }
     }
     if (fill) run(fill);
+#pragma unroll
+    for (int a = 0; a < K::KT; ++a) acc[a] += acc2[a];
     slice_reduce_store<K::KT>(z, acc, red, outs + t0 * K::KT, true);
   }
 }
@@ -303,12 +322,13 @@ __global__ void k_scatter(const double* __restrict__ outs, const int64_t* __rest
   out[perm[i] * kt + c] = scale * outs[t];
 }
 
-__global__ void k_check_values(const double* __restrict__ v, int64_t n, int ks, int* flag) {
+// pcol: column of the per-source parameter (b or eps, must be >= 0), or -1
+__global__ void k_check_values(const double* __restrict__ v, int64_t n, int ks, int pcol, int* flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n * ks) return;
   double x = v[t];
   if (!isfinite(x)) atomicOr(flag, 2);
-  if (ks == 4 && (t % 4) == 3 && x < 0.0) atomicOr(flag, 2);
+  if (pcol >= 0 && (t % ks) == pcol && x < 0.0) atomicOr(flag, 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -418,6 +438,7 @@ void run_eval_up(Plan& P, const double* d_src) {
     case KAFMM_STOKESLET: eval_up_impl<KG, 8>(P, d_src); break;
     case KAFMM_RPY: eval_up_impl<KRPY, 8>(P, d_src); break;
     case KAFMM_STOKES_REG_VEL: eval_up_impl<KGE, 8>(P, d_src); break;
+    case KAFMM_STOKES_REG_VEL_OMEGA: eval_up_impl<KGET, 12>(P, d_src); break;
     default: throw Error{KAFMM_EINVAL, "unknown kernel"};
   }
 }
@@ -428,6 +449,7 @@ void run_eval_down(Plan& P, double* d_out) {
     case KAFMM_STOKESLET: eval_down_impl<KG, KG, KG, 8>(P, d_out); break;
     case KAFMM_RPY: eval_down_impl<KRPY, KGL, KRPYL, 8>(P, d_out); break;
     case KAFMM_STOKES_REG_VEL: eval_down_impl<KGE, KG, KGE, 8>(P, d_out); break;
+    case KAFMM_STOKES_REG_VEL_OMEGA: eval_down_impl<KGET, KGO, KGETW, 12>(P, d_out); break;
     default: throw Error{KAFMM_EINVAL, "unknown kernel"};
   }
 }
@@ -439,7 +461,8 @@ void run_eval(Plan& P, const double* d_src, double* d_out) {
 
 void check_values(Plan& P, const double* d_src) {
   KF_CUDA(cudaMemsetAsync(P.d_flag, 0, 4, P.stream));
-  k_check_values<<<nblk(P.n * P.ks), 256, 0, P.stream>>>(d_src, P.n, P.ks, P.d_flag);
+  const int pcol = P.ks == 4 ? 3 : (P.ks == 7 ? 6 : -1);
+  k_check_values<<<nblk(P.n * P.ks), 256, 0, P.stream>>>(d_src, P.n, P.ks, pcol, P.d_flag);
   KF_CHECK_LAUNCH();
   int h = 0;
   KF_CUDA(cudaMemcpyAsync(&h, P.d_flag, 4, cudaMemcpyDeviceToHost, P.stream));

@@ -114,7 +114,7 @@ template <int P>
 __global__ void __launch_bounds__(256)
     k_fft_fwd(const int32_t* __restrict__ qbox, const int32_t* __restrict__ child, int64_t nq,
               const double* __restrict__ ue, int ldn, int kml, const int16_t* __restrict__ lat, int M,
-              double2* __restrict__ ub) {
+              double2* __restrict__ ub, int zero_missing) {
   using D = FftDims<P>;
   constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF;
   constexpr int GZ = (NZ + FT - 1) / FT, GG = (NG + FT - 1) / FT;
@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(256)
   const int c = blockIdx.x & 7, tid = threadIdx.x, bd = blockDim.x;
   const int R = 8 * kml;
   const int64_t box = child[8 * (int64_t)qbox[q] + c];
-  if (box < 0) {
+  if (box < 0) {  // the per-pair product never reads a missing child: zeros only for blocks
+    if (!zero_missing) return;
     for (int e = 0; e < kml; ++e)
       for (int f = tid; f < NF; f += bd) ub[((int64_t)f * nq + q) * R + c * kml + e] = make_double2(0.0, 0.0);
     return;
@@ -428,10 +429,13 @@ __global__ void __launch_bounds__(PAIR_THREADS)
                 const double2* __restrict__ ub, double2* __restrict__ cb, const int2* __restrict__ tpb,
                 const int64_t* __restrict__ off, const int32_t* __restrict__ pl) {
   constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
-  __shared__ double2 sT[N_OFFSETS * NC];
+  // operator spectra of this frequency as NC planes of 316 complex: lanes that
+  // gather different offsets spread over 8 bank groups (a 96-B record stride
+  // would hit only 4)
+  __shared__ double2 sT[NC][N_OFFSETS];
   const int64_t f = blockIdx.x / ntb;
   const int tb = blockIdx.x % ntb;
-  for (int i = threadIdx.x; i < N_OFFSETS * NC; i += PAIR_THREADS) sT[i] = that[f * N_OFFSETS * NC + i];
+  for (int i = threadIdx.x; i < N_OFFSETS * NC; i += PAIR_THREADS) sT[i % NC][i / NC] = that[f * N_OFFSETS * NC + i];
   __syncthreads();
   const int64_t t = (int64_t)tb * PAIR_THREADS + threadIdx.x;
   if (t >= nt) return;
@@ -439,25 +443,40 @@ __global__ void __launch_bounds__(PAIR_THREADS)
   double2 acc[KML];
 #pragma unroll
   for (int a = 0; a < KML; ++a) acc[a] = make_double2(0.0, 0.0);
+  // pairs in batches of PB: their source spectra are loaded together (memory
+  // level parallelism), then the products run from registers
+  constexpr int PB = 4;
   const int64_t e1 = off[t + 1];
-  for (int64_t e = off[t]; e < e1; ++e) {
-    const int v = pl[e];
-    const double2* u = ubf + (int64_t)(v >> 9) * KML;
-    const double2* T = sT + (v & 511) * NC;
-    if (KML == 1) {
-      cmac(acc[0], T[0], u[0]);
-    } else {
-      const double2 u0 = u[0], u1 = u[1], u2 = u[2];
-      const double2 t0 = T[0], t1 = T[1], t2 = T[2], t3 = T[3], t4 = T[4], t5 = T[5];
-      cmac(acc[0], t0, u0);
-      cmac(acc[0], t1, u1);
-      cmac(acc[0], t2, u2);
-      cmac(acc[KML > 1 ? 1 : 0], t1, u0);
-      cmac(acc[KML > 1 ? 1 : 0], t3, u1);
-      cmac(acc[KML > 1 ? 1 : 0], t4, u2);
-      cmac(acc[KML > 2 ? 2 : 0], t2, u0);
-      cmac(acc[KML > 2 ? 2 : 0], t4, u1);
-      cmac(acc[KML > 2 ? 2 : 0], t5, u2);
+  for (int64_t e = off[t]; e < e1; e += PB) {
+    int v[PB];
+    double2 u[PB][KML];
+#pragma unroll
+    for (int j = 0; j < PB; ++j) v[j] = e + j < e1 ? pl[e + j] : -1;
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+      const double2* up = ubf + (int64_t)(v[j] >> 9) * KML;
+#pragma unroll
+      for (int a = 0; a < KML; ++a) u[j][a] = v[j] >= 0 ? up[a] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+      const int o = v[j] >= 0 ? (v[j] & 511) : 0;
+      if (KML == 1) {
+        cmac(acc[0], sT[0][o], u[j][0]);
+      } else {
+        const double2 t0 = sT[0][o], t1 = sT[NC > 1 ? 1 : 0][o], t2 = sT[NC > 2 ? 2 : 0][o],
+                      t3 = sT[NC > 3 ? 3 : 0][o], t4 = sT[NC > 4 ? 4 : 0][o], t5 = sT[NC > 5 ? 5 : 0][o];
+        const double2 u0 = u[j][0], u1 = u[j][KML > 1 ? 1 : 0], u2 = u[j][KML > 2 ? 2 : 0];
+        cmac(acc[0], t0, u0);
+        cmac(acc[0], t1, u1);
+        cmac(acc[0], t2, u2);
+        cmac(acc[KML > 1 ? 1 : 0], t1, u0);
+        cmac(acc[KML > 1 ? 1 : 0], t3, u1);
+        cmac(acc[KML > 1 ? 1 : 0], t4, u2);
+        cmac(acc[KML > 2 ? 2 : 0], t2, u0);
+        cmac(acc[KML > 2 ? 2 : 0], t4, u1);
+        cmac(acc[KML > 2 ? 2 : 0], t5, u2);
+      }
     }
   }
   const int2 pb = tpb[t];
@@ -480,11 +499,15 @@ static void set_smem_attrs() {
   done = true;
 }
 
+static bool chunk_uses_pairs(const Plan& Pl, const FftChunk& ch) {
+  return Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < FFT_PAIR_FILL);
+}
+
 template <int P>
 static void launch_fwd(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
   k_fft_fwd<P><<<(unsigned)(8 * ch.nq), 256, FftDims<P>::FWD_SMEM, Pl.stream>>>(
-      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lat, Pl.M, Pl.d_ub);
+      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lat, Pl.M, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1);
   KF_CHECK_LAUNCH();
   Pl.launches++;
 }
@@ -518,7 +541,7 @@ void run_m2l_fft(Plan& Pl) {
   for (const FftChunk& ch : Pl.fft_chunks) {
     if (ch.nt == 0 || ch.nq == 0) continue;
     KF_FFT_DISPATCH(launch_fwd);
-    const bool pairs = Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < FFT_PAIR_FILL);
+    const bool pairs = chunk_uses_pairs(Pl, ch);
     prod_mark(Pl);
     if (pairs) {
       const int ntb = (int)((ch.nt + PAIR_THREADS - 1) / PAIR_THREADS);

@@ -38,9 +38,11 @@ CASES = [
     ("stokeslet_spheres", "stokeslet", lambda: WL.make_points(WL.CONFIGS[5], 12000, n_spheres=60), 6, 64),
     # polydisperse b / eps on the paper's log-normal cloud (C6, C7 shapes)
     ("C6_poly_rpy", "rpy", lambda: WL.make_points(WL.CONFIGS[6], 12000), 8, 150),
-    ("C7_poly_regvel", "stokes_reg_vel", lambda: WL.make_points(WL.CONFIGS[7], 12000), 8, 150),
+    ("C7_poly_regvel_omega", "stokes_reg_vel_omega", lambda: WL.make_points(WL.CONFIGS[7], 12000), 8, 150),
+    # StokesRegVelOmega (Table VI) on an adaptive tree
+    ("regvel_omega_clustered", "stokes_reg_vel_omega", lambda: _clustered(4000, 7), 6, 32),
 ]
-POLY = {"C6_poly_rpy": 6, "C7_poly_regvel": 7}
+POLY = {"C6_poly_rpy": 6, "C7_poly_regvel_omega": 7}
 
 
 @pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])

@@ -198,3 +198,78 @@ def test_direct_sum_two_opposite_charges_and_scalar_loop():
             for j in range(11):
                 ref[i] += pair_values(name, X[i] - Y[j], vv[j])
         np.testing.assert_allclose(direct_sum(name, X, Y, vv), ref, rtol=1e-13, atol=1e-13)
+
+
+# ---- StokesRegVelOmega, Table VI --------------------------
+def _ft(rng):
+    return rng.standard_normal(3), rng.standard_normal(3)
+
+
+def _curl(fun, x, h=1e-5):
+    J = np.zeros((3, 3))
+    for k in range(3):
+        e = np.zeros(3)
+        e[k] = h
+        J[:, k] = (fun(x + e) - fun(x - e)) / (2 * h)
+    return np.array([J[2, 1] - J[1, 2], J[0, 2] - J[2, 0], J[1, 0] - J[0, 1]])
+
+
+@pytest.mark.parametrize("eps", [0.0, 0.3, 1.0])
+def test_reg_vel_omega_is_half_curl_of_velocity(eps):
+    # omega = (1/2) curl u for both the force and the torque parts (Omega = curl G / 2,
+    # W = curl T / 2): a property of the blob-regularized flows, not of how they are coded
+    rng = np.random.default_rng(21)
+    for _ in range(3):
+        r = rng.standard_normal(3)
+        f, t = _ft(rng)
+        for s in (np.concatenate([f, 0 * t, [eps]]), np.concatenate([0 * f, t, [eps]])):
+            u = lambda x: pair_values("G_eps+Omega+T+W", x, s)[:3]  # noqa: E731
+            w = pair_values("G_eps+Omega+T+W", r, s)[3:]
+            np.testing.assert_allclose(w, 0.5 * _curl(u, r), rtol=1e-7, atol=1e-9)
+
+
+def test_reg_vel_omega_limits_and_pieces():
+    rng = np.random.default_rng(22)
+    r = rng.standard_normal((50, 3))
+    f = rng.standard_normal((50, 3))
+    t = rng.standard_normal((50, 3))
+    eps = 0.2 * rng.random(50)
+    s7 = np.concatenate([f, t, eps[:, None]], axis=1)
+    full = pair_values("G_eps+Omega+T+W", r, s7)
+    # S-row kernel = the velocity block of the S->T kernel
+    np.testing.assert_array_equal(pair_values("G_eps+T_eps", r, s7), full[:, :3])
+    # no torque: the velocity is the regularized Stokeslet G_eps
+    s0 = np.concatenate([f, 0 * t, eps[:, None]], axis=1)
+    np.testing.assert_allclose(pair_values("G_eps+Omega+T+W", r, s0)[:, :3],
+                               pair_values("G_eps", r, np.concatenate([f, eps[:, None]], axis=1)), rtol=1e-14)
+    # eps -> 0 with no torque is the singular G (+) Omega of the T column
+    z = np.concatenate([f, 0 * t, 0 * eps[:, None]], axis=1)
+    np.testing.assert_allclose(pair_values("G_eps+Omega+T+W", r, z), pair_values("G+Omega", r, f), rtol=1e-13)
+
+
+def test_reg_vel_omega_worked_values_and_self_term():
+    # r = (1,0,0), eps = 0, torque t = (0,0,1): u = Q/2 (t x r), Q(1) = 2/(8 pi) -> u = (0, 1/(8 pi), 0)
+    s = np.array([0, 0, 0, 0, 0, 1.0, 0.0])
+    np.testing.assert_allclose(pair_values("G_eps+Omega+T+W", np.array([1.0, 0, 0]), s)[:3],
+                               [0, 1 / (8 * np.pi), 0], atol=1e-17)
+    # self term r = 0: H1(0) = 1/(4 pi eps), D1(0)/4 = 10/(32 pi eps^3), Q-terms vanish
+    eps = 0.5
+    f, t = np.array([1.0, 2, 3]), np.array([-1.0, 0.5, 2])
+    got = pair_values("G_eps+Omega+T+W", np.zeros(3), np.concatenate([f, t, [eps]]))
+    np.testing.assert_allclose(got[:3], f / (4 * np.pi * eps), rtol=1e-15)
+    np.testing.assert_allclose(got[3:], 10 * t / (32 * np.pi * eps ** 3), rtol=1e-15)
+
+
+def test_reg_vel_omega_mobility_is_symmetric():
+    # two blobs with the same eps: the 12x12 mobility [u1, w1, u2, w2] <- [f1, t1, f2, t2] is symmetric
+    rng = np.random.default_rng(23)
+    x = rng.standard_normal((2, 3))
+    eps = 0.3
+    Mb = np.zeros((12, 12))
+    for j in range(12):
+        s = np.zeros((2, 7))
+        s[:, 6] = eps
+        s[j // 6, j % 6] = 1.0
+        for a in range(2):
+            Mb[6 * a:6 * a + 6, j] = sum(pair_values("G_eps+Omega+T+W", x[a] - x[b], s[b]) for b in range(2))
+    np.testing.assert_allclose(Mb, Mb.T, rtol=0, atol=1e-14)

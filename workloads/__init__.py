@@ -23,7 +23,8 @@ Recipe:
           u - [u] with u log-normal (m = -1, s = 0.5), i.e. the paper's
           L (u - [u]) with L = 32 scaled to the unit cube; N = 10^6, leaf cap
           2000, values U[-1, 1], polydisperse
-          b (C6, RPY) or eps (C7, RegVel) iid U[0, 1e-4] in the paper's units
+          b (C6, RPY [f, b] -> [u, lap u]) or eps (C7, StokesRegVelOmega
+          [f, t, eps] -> [u, omega], Table VI) iid U[0, 1e-4] in the paper's units
           (PAPER.md:676), i.e. U[0, 1e-4 / 32] in the unit cube; p = 10
 The BASELINE configs are the paper-shaped stand-ins for the paper's own
 synthetic clouds (Eq. (ptdist)); no dataset is involved.
@@ -35,11 +36,14 @@ import numpy as np
 
 SEED_ROOT = 201015155
 
-KERNELS = ("laplace_pgrad", "stokeslet", "rpy", "stokes_reg_vel")
+KERNELS = ("laplace_pgrad", "stokeslet", "rpy", "stokes_reg_vel", "stokes_reg_vel_omega")
 # (k_s, k_t) per kernel: PAPER.md Table XI (lines 874-880)
-KERNEL_DIMS = {"laplace_pgrad": (1, 4), "stokeslet": (3, 3), "rpy": (4, 6), "stokes_reg_vel": (4, 3)}
+KERNEL_DIMS = {"laplace_pgrad": (1, 4), "stokeslet": (3, 3), "rpy": (4, 6), "stokes_reg_vel": (4, 3),
+               "stokes_reg_vel_omega": (7, 6)}
 # C-ABI enum values (include/kafmm.h)
-KERNEL_ENUM = {"laplace_pgrad": 1, "stokeslet": 2, "rpy": 3, "stokes_reg_vel": 4}
+KERNEL_ENUM = {"laplace_pgrad": 1, "stokeslet": 2, "rpy": 3, "stokes_reg_vel": 4, "stokes_reg_vel_omega": 5}
+# source column of the nonlinear per-source parameter (b or eps), if any
+PARAM_COL = {"rpy": 3, "stokes_reg_vel": 3, "stokes_reg_vel_omega": 6}
 
 
 @dataclasses.dataclass(frozen=True)
@@ -65,7 +69,7 @@ CONFIGS = {
     4: ConfigSpec(4, "stokes_reg_vel", 8_000_000, 12, 64, "clusters", 1e-4),
     5: ConfigSpec(5, "stokeslet", 64_000_000, 8, 128, "spheres"),
     6: ConfigSpec(6, "rpy", 1_000_000, 10, 2000, "lognormal", 1e-4 / 32, True),
-    7: ConfigSpec(7, "stokes_reg_vel", 1_000_000, 10, 2000, "lognormal", 1e-4 / 32, True),
+    7: ConfigSpec(7, "stokes_reg_vel_omega", 1_000_000, 10, 2000, "lognormal", 1e-4 / 32, True),
 }
 LOGNORMAL_M, LOGNORMAL_S = -1.0, 0.5
 
@@ -164,7 +168,7 @@ def make_values(spec: ConfigSpec, n: int | None = None):
     k_s = KERNEL_DIMS[spec.kernel][0]
     if spec.poly:
         vals = rv.uniform(-1.0, 1.0, size=(n, k_s))
-        vals[:, 3] = rv.uniform(0.0, spec.extra, size=n)
+        vals[:, PARAM_COL[spec.kernel]] = rv.uniform(0.0, spec.extra, size=n)
     elif spec.kernel == "laplace_pgrad":
         vals = rv.standard_normal((n, 1))
     elif spec.kernel == "stokeslet":
@@ -193,6 +197,6 @@ def random_values(kernel: str, n: int, seed: int, extra: float | None = None):
     rng = np.random.default_rng(seed)
     k_s = KERNEL_DIMS[kernel][0]
     v = rng.standard_normal((n, k_s))
-    if k_s == 4:
-        v[:, 3] = (1e-3 if kernel == "rpy" else 1e-4) if extra is None else extra
+    if kernel in PARAM_COL:
+        v[:, PARAM_COL[kernel]] = (1e-3 if kernel == "rpy" else 1e-4) if extra is None else extra
     return v
