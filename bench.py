@@ -38,7 +38,8 @@ sys.path.insert(0, ROOT)
 import workloads as WL  # noqa: E402
 
 # nominal flops per pair of the P2P kernels (rsqrt counted as 8)
-P2P_FLOPS = {"laplace_pgrad": 27, "stokeslet": 36, "rpy": 56, "stokes_reg_vel": 39, "stokes_reg_vel_omega": 100}
+P2P_FLOPS = {"laplace_pgrad": 27, "stokeslet": 36, "rpy": 56, "stokes_reg_vel": 39, "stokes_reg_vel_omega": 100,
+             "laplace_pgradgrad": 90, "laplace_qpgradgrad": 120}
 
 
 def parse():

@@ -57,6 +57,11 @@ typedef enum {
  *   STOKES_REG_VEL_OMEGA  k_s=7 [f, t, eps]  k_t=6 [u, omega]:
  *                   u = sum G^eps f + T^eps t, omega = sum Omega^eps f + W^eps t
  *                   (Table VI; ML tree G, T column G (+) Omega)
+ *   LAPLACE_PGRADGRAD  k_s=4 [q, d]  k_t=10 [phi, grad phi, grad grad phi (xx,xy,xz,yy,yz,zz)]
+ *                   charges and dipoles at every point, phi = sum (q + d . grad_y)/(4 pi r)
+ *                   (Table III; ML tree L)
+ *   LAPLACE_QPGRADGRAD k_s=9 [Q (3x3 row-major)]  k_t=10 as LAPLACE_PGRADGRAD,
+ *                   phi = sum Q_jk d2/dx_j dx_k 1/(4 pi r) (Table XI)
  * Self pairs (r^2 == 0) are skipped by the singular kernels and kept by the
  * regularized ones, where G^eps(0) = 1/(4 pi eps) is finite. */
 typedef enum {
@@ -64,7 +69,9 @@ typedef enum {
   KAFMM_STOKESLET = 2,
   KAFMM_RPY = 3,
   KAFMM_STOKES_REG_VEL = 4,
-  KAFMM_STOKES_REG_VEL_OMEGA = 5
+  KAFMM_STOKES_REG_VEL_OMEGA = 5,
+  KAFMM_LAPLACE_PGRADGRAD = 6,
+  KAFMM_LAPLACE_QPGRADGRAD = 7
 } kafmm_kernel;
 
 /* Source and target dimensions of a kernel.  EINVAL for an unknown kernel. */

@@ -8,6 +8,8 @@ Kernel tables (which kernel each of the 8 traversal stages uses):
   RPY       Table IV: S-row G_RPY, ML tree G,
             T column G+lapG, S2T G_RPY+lapG
   RegVel    Table V: S-row G_eps, ML tree and T column G
+  LapPGradGrad Table III: S-row L (charges) and L^D (dipoles),
+            ML tree L, T column L+gradL+gradgradL, S2T the same from [q, d]
   RegVelOmega Table VI: S-row G_eps+T_eps, ML tree G,
             T column G+Omega, S2T G_eps+Omega+T+W
 
@@ -42,6 +44,10 @@ TABLES = {
     "stokes_reg_vel": dict(S="G_eps", ML="G", T="G", ST="G_eps"),
     # Table VI: [f, t, eps] -> [u, omega]
     "stokes_reg_vel_omega": dict(S="G_eps+T_eps", ML="G", T="G+Omega", ST="G_eps+Omega+T+W"),
+    # Table III: charges and dipoles [q, d] -> [phi, grad, grad grad]
+    "laplace_pgradgrad": dict(S="L+LD", ML="L", T="L+gradL+gradgradL", ST="LD+gradLD+gradgradLD"),
+    # LapQPGradGrad (Table XI; same pattern as Table III with quadrupoles)
+    "laplace_qpgradgrad": dict(S="LQ", ML="L", T="L+gradL+gradgradL", ST="LQ+gradLQ+gradgradLQ"),
 }
 
 _OPS_CACHE: dict = {}
@@ -237,4 +243,6 @@ def blocks(kernel: str):
     """Output blocks per reading R11 (phi | grad phi ; u | lap u)."""
     return {"laplace_pgrad": [(0, 1), (1, 4)], "stokeslet": [(0, 3)],
             "rpy": [(0, 3), (3, 6)], "stokes_reg_vel": [(0, 3)],
-            "stokes_reg_vel_omega": [(0, 3), (3, 6)]}[kernel]
+            "stokes_reg_vel_omega": [(0, 3), (3, 6)],
+            "laplace_pgradgrad": [(0, 1), (1, 4), (4, 10)],
+            "laplace_qpgradgrad": [(0, 1), (1, 4), (4, 10)]}[kernel]

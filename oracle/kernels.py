@@ -12,6 +12,13 @@ Kernel names follow the paper's notation:
   G_RPY+lapG [u, lap u]; lap G^RPY = lap G since lap lap G = 0
   G+lapG     [u, lap u] from point forces                          PAPER.md:106, Table IV
   G_eps      regularized Stokeslet
+  L+LD       [q, d] -> phi = q L + d . L^D, L^D_j = -dL/dx_j = r_j/(4 pi r^3)   PAPER.md:215-221, Table III S row
+  L+gradL+gradgradL    q -> [phi, grad phi, grad grad phi]         Table III T column (ML-tree charges)
+  LD+gradLD+gradgradLD [q, d] -> [phi, grad phi, grad grad phi]  Table III S->T (charges and dipoles)
+      grad grad phi as (xx, xy, xz, yy, yz, zz)
+  LQ         Q -> phi = Q_jk L^Q_jk, L^Q_jk = d2 L/dx_j dx_k                  PAPER.md:218-221 (LapQPGradGrad S row)
+  LQ+gradLQ+gradgradLQ  Q -> [phi, grad phi, grad grad phi]             LapQPGradGrad S->T (Table XI)
+      Q a general 3x3 matrix, row-major (Q_xx, Q_xy, Q_xz, Q_yx, ...)
   G_eps+T_eps            [f, t, eps] -> u = G^eps f + T^eps t        Table VI S-row, PAPER.md:357-362
   G+Omega                f -> [u, omega] = [G f, Omega f] (eps = 0)  Table VI T column
   G_eps+Omega+T+W        [f, t, eps] -> [u, omega], the 7x6 S->T     PAPER.md:356-374, Table VI
@@ -40,12 +47,18 @@ DIMS = {
     "G_RPY+lapG": (4, 6),
     "G+lapG": (3, 6),
     "G_eps": (4, 3),
+    "L+LD": (4, 1),
+    "LQ": (9, 1),
+    "LQ+gradLQ+gradgradLQ": (9, 10),
+    "L+gradL+gradgradL": (1, 10),
+    "LD+gradLD+gradgradLD": (4, 10),
     "G_eps+T_eps": (7, 3),
     "G+Omega": (3, 6),
     "G_eps+Omega+T+W": (7, 6),
 }
 SINGULAR = {"L": True, "L+gradL": True, "G": True, "G_RPY": True, "G_RPY+lapG": True,
-            "G+lapG": True, "G_eps": False, "G_eps+T_eps": False, "G+Omega": True,
+            "G+lapG": True, "G_eps": False, "L+LD": True, "L+gradL+gradgradL": True,
+            "LD+gradLD+gradgradLD": True, "LQ": True, "LQ+gradLQ+gradgradLQ": True, "G_eps+T_eps": False, "G+Omega": True,
             "G_eps+Omega+T+W": False}
 
 
@@ -96,6 +109,54 @@ def pair_values(name: str, r: np.ndarray, s: np.ndarray) -> np.ndarray:
         phi = q * rinv / FOUR_PI
         grad = -(q * rinv3)[..., None] * r / FOUR_PI
         return np.concatenate([phi[..., None], grad], axis=-1)
+    if name in ("LQ", "LQ+gradLQ+gradgradLQ"):
+        # derivatives of 1/r contracted with Q_jk:
+        #   d_j d_k     3 r_j r_k / r^5 - delta_jk / r^3
+        #   d_i d_j d_k -15 r_i r_j r_k / r^7 + 3 (delta_ij r_k + delta_ik r_j + delta_jk r_i) / r^5
+        #   d_i d_l d_j d_k  105 r_i r_j r_k r_l / r^9 - 15 (6 delta r r terms) / r^7 + 3 (3 delta delta) / r^5
+        Q = s.reshape(s.shape[:-1] + (3, 3))
+        rinv5 = rinv3 * rinv * rinv
+        rinv7 = rinv5 * rinv * rinv
+        rinv9 = rinv7 * rinv * rinv
+        a = np.einsum("...j,...jk,...k->...", r, Q, r)
+        tq = np.trace(Q, axis1=-2, axis2=-1)
+        w = np.einsum("...ik,...k->...i", Q, r) + np.einsum("...ji,...j->...i", Q, r)
+        phi = 3.0 * a * rinv5 - tq * rinv3
+        if name == "LQ":
+            return (phi / FOUR_PI)[..., None]
+        grad = (-15.0 * a * rinv7)[..., None] * r + 3.0 * rinv5[..., None] * (w + tq[..., None] * r)
+        I = np.eye(3)
+        rr = r[..., :, None] * r[..., None, :]
+        hess = ((105.0 * a * rinv9)[..., None, None] * rr
+                - 15.0 * rinv7[..., None, None] * (a[..., None, None] * I + r[..., None, :] * w[..., :, None]
+                                                   + r[..., :, None] * w[..., None, :] + tq[..., None, None] * rr)
+                + 3.0 * rinv5[..., None, None] * (tq[..., None, None] * I + Q + np.swapaxes(Q, -1, -2)))
+        iu = ([0, 0, 0, 1, 1, 2], [0, 1, 2, 1, 2, 2])
+        return np.concatenate([phi[..., None], grad, hess[..., iu[0], iu[1]]], axis=-1) / FOUR_PI
+    if name in ("L+LD", "L+gradL+gradgradL", "LD+gradLD+gradgradLD"):
+        q = s[..., 0]
+        rinv5 = rinv3 * rinv * rinv
+        # charge: phi = q/r, grad = -q r/r^3, grad grad_jk = q (3 r_j r_k/r^5 - delta_jk/r^3)
+        phi = q * rinv
+        grad = -(q * rinv3)[..., None] * r
+        hess = q[..., None, None] * (3.0 * rinv5[..., None, None] * r[..., :, None] * r[..., None, :]
+                                     - rinv3[..., None, None] * np.eye(3))
+        if name != "L+gradL+gradgradL":
+            # dipole: phi = d.r/r^3 (L^D_j = r_j/(4 pi r^3)), grad = d/r^3 - 3 (d.r) r/r^5,
+            # grad grad_jk = -3 (d_j r_k + d_k r_j + (d.r) delta_jk)/r^5 + 15 (d.r) r_j r_k/r^7
+            d = s[..., 1:4]
+            dr = np.sum(d * r, axis=-1)
+            rinv7 = rinv5 * rinv * rinv
+            phi = phi + dr * rinv3
+            if name == "L+LD":
+                return (phi / FOUR_PI)[..., None]
+            grad = grad + rinv3[..., None] * d - (3.0 * dr * rinv5)[..., None] * r
+            hess = hess + (-3.0 * rinv5[..., None, None] * (d[..., :, None] * r[..., None, :]
+                                                            + r[..., :, None] * d[..., None, :]
+                                                            + dr[..., None, None] * np.eye(3))
+                           + (15.0 * dr * rinv7)[..., None, None] * r[..., :, None] * r[..., None, :])
+        iu = ([0, 0, 0, 1, 1, 2], [0, 1, 2, 1, 2, 2])
+        return np.concatenate([phi[..., None], grad, hess[..., iu[0], iu[1]]], axis=-1) / FOUR_PI
     f = s[..., :3]
     rf = np.sum(r * f, axis=-1)
     if name == "G":

@@ -20,6 +20,8 @@ static int dims(int kernel, int* ks, int* kt) {
     case KAFMM_RPY: *ks = 4; *kt = 6; return 0;
     case KAFMM_STOKES_REG_VEL: *ks = 4; *kt = 3; return 0;
     case KAFMM_STOKES_REG_VEL_OMEGA: *ks = 7; *kt = 6; return 0;
+    case KAFMM_LAPLACE_PGRADGRAD: *ks = 4; *kt = 10; return 0;
+    case KAFMM_LAPLACE_QPGRADGRAD: *ks = 9; *kt = 10; return 0;
     default: return -1;
   }
 }
@@ -103,8 +105,10 @@ kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int
   P->n = n;
   P->ks = ks;
   P->kt = kt;
-  P->kml = (kernel == KAFMM_LAPLACE_PGRAD) ? 1 : 3;
-  P->srec = (kernel == KAFMM_LAPLACE_PGRAD) ? 4 : (kernel == KAFMM_STOKES_REG_VEL_OMEGA ? 12 : 8);
+  const bool laplace =
+      kernel == KAFMM_LAPLACE_PGRAD || kernel == KAFMM_LAPLACE_PGRADGRAD || kernel == KAFMM_LAPLACE_QPGRADGRAD;
+  P->kml = laplace ? 1 : 3;
+  P->srec = (3 + ks + 3) / 4 * 4;  // x, y, z + source values, padded to 32 bytes
   P->M = 6 * (p - 1) * (p - 1) + 2;
   P->neq = P->kml * P->M;
   P->ldn = round_up(P->neq, GEMM_BK);

@@ -421,7 +421,7 @@ static void eval_down_impl(Plan& P, double* d_out) {
     P.launches++;
   }
   mark(ST_SCATTER);
-  const double scale = (P.kernel == KAFMM_LAPLACE_PGRAD) ? 1.0 / (4.0 * M_PI) : 1.0 / (8.0 * M_PI);
+  const double scale = (P.kml == 1) ? 1.0 / (4.0 * M_PI) : 1.0 / (8.0 * M_PI);
   const int64_t cnt = (J.phi - J.plo) * P.kt;
   if (cnt > 0) {
     k_scatter<<<nblk(cnt), 256, 0, st>>>(P.d_outs + J.plo * P.kt, P.d_perm + J.plo, J.phi - J.plo, P.kt, scale,
@@ -439,6 +439,8 @@ void run_eval_up(Plan& P, const double* d_src) {
     case KAFMM_RPY: eval_up_impl<KRPY, 8>(P, d_src); break;
     case KAFMM_STOKES_REG_VEL: eval_up_impl<KGE, 8>(P, d_src); break;
     case KAFMM_STOKES_REG_VEL_OMEGA: eval_up_impl<KGET, 12>(P, d_src); break;
+    case KAFMM_LAPLACE_PGRADGRAD: eval_up_impl<KLD, 8>(P, d_src); break;
+    case KAFMM_LAPLACE_QPGRADGRAD: eval_up_impl<KLQ, 12>(P, d_src); break;
     default: throw Error{KAFMM_EINVAL, "unknown kernel"};
   }
 }
@@ -450,6 +452,8 @@ void run_eval_down(Plan& P, double* d_out) {
     case KAFMM_RPY: eval_down_impl<KRPY, KGL, KRPYL, 8>(P, d_out); break;
     case KAFMM_STOKES_REG_VEL: eval_down_impl<KGE, KG, KGE, 8>(P, d_out); break;
     case KAFMM_STOKES_REG_VEL_OMEGA: eval_down_impl<KGET, KGO, KGETW, 12>(P, d_out); break;
+    case KAFMM_LAPLACE_PGRADGRAD: eval_down_impl<KLD, KLGG, KLDGG, 8>(P, d_out); break;
+    case KAFMM_LAPLACE_QPGRADGRAD: eval_down_impl<KLQ, KLGG, KLQGG, 12>(P, d_out); break;
     default: throw Error{KAFMM_EINVAL, "unknown kernel"};
   }
 }
@@ -461,7 +465,8 @@ void run_eval(Plan& P, const double* d_src, double* d_out) {
 
 void check_values(Plan& P, const double* d_src) {
   KF_CUDA(cudaMemsetAsync(P.d_flag, 0, 4, P.stream));
-  const int pcol = P.ks == 4 ? 3 : (P.ks == 7 ? 6 : -1);
+  const int pcol = (P.kernel == KAFMM_RPY || P.kernel == KAFMM_STOKES_REG_VEL) ? 3
+                   : (P.kernel == KAFMM_STOKES_REG_VEL_OMEGA ? 6 : -1);
   k_check_values<<<nblk(P.n * P.ks), 256, 0, P.stream>>>(d_src, P.n, P.ks, pcol, P.d_flag);
   KF_CHECK_LAUNCH();
   int h = 0;

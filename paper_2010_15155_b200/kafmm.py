@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-KERNELS = {"laplace_pgrad": 1, "stokeslet": 2, "rpy": 3, "stokes_reg_vel": 4, "stokes_reg_vel_omega": 5}
+KERNELS = {"laplace_pgrad": 1, "stokeslet": 2, "rpy": 3, "stokes_reg_vel": 4, "stokes_reg_vel_omega": 5,
+           "laplace_pgradgrad": 6, "laplace_qpgradgrad": 7}
 N_STAGES = 13
 
 

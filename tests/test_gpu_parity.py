@@ -41,8 +41,12 @@ CASES = [
     ("C7_poly_regvel_omega", "stokes_reg_vel_omega", lambda: WL.make_points(WL.CONFIGS[7], 12000), 8, 150),
     # StokesRegVelOmega (Table VI) on an adaptive tree
     ("regvel_omega_clustered", "stokes_reg_vel_omega", lambda: _clustered(4000, 7), 6, 32),
+    # LapPGradGrad (Table III), charges + dipoles on the paper's cloud (C8 shape)
+    ("C8_pgradgrad", "laplace_pgradgrad", lambda: WL.make_points(WL.CONFIGS[8], 12000), 8, 150),
+    ("pgradgrad_clustered", "laplace_pgradgrad", lambda: _clustered(5000, 8), 7, 30),
+    ("C9_qpgradgrad", "laplace_qpgradgrad", lambda: WL.make_points(WL.CONFIGS[9], 12000), 8, 150),
 ]
-POLY = {"C6_poly_rpy": 6, "C7_poly_regvel_omega": 7}
+POLY = {"C6_poly_rpy": 6, "C7_poly_regvel_omega": 7, "C8_pgradgrad": 8, "C9_qpgradgrad": 9}
 
 
 @pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])

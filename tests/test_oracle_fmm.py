@@ -48,7 +48,8 @@ def test_zero_sources_and_superposition(kernel):
 
 
 @pytest.mark.parametrize("kernel,ps", [("laplace_pgrad", (4, 6, 8, 10)), ("stokeslet", (4, 6, 8)),
-                                       ("stokes_reg_vel_omega", (4, 6, 8))])
+                                       ("stokes_reg_vel_omega", (4, 6, 8)), ("laplace_pgradgrad", (4, 6, 8)),
+                                       ("laplace_qpgradgrad", (4, 6, 8))])
 def test_error_decreases_with_p(kernel, ps):
     # PAPER.md:646 / :679 "as m linearly increases, the convergence error exponentially decreases"
     pts, vals = _cloud(1500, 3, kernel)
@@ -97,9 +98,15 @@ def test_scale_covariance_is_exact(kernel):
         v2[:, WL.PARAM_COL[kernel]] *= 0.5
     if kernel == "stokes_reg_vel_omega":
         v2[:, 3:6] *= 0.5
+    if kernel == "laplace_pgradgrad":  # dipole potential has degree -2: scale d with x
+        v2[:, 1:4] *= 0.5
+    if kernel == "laplace_qpgradgrad":  # quadrupole potential has degree -3
+        v2 *= 0.25
     b = F.fmm(pts * 0.5, v2, kernel, 5, 30)["out"]
     scale = {"laplace_pgrad": [2, 4, 4, 4], "stokeslet": [2] * 3, "rpy": [2] * 3 + [8] * 3,
-             "stokes_reg_vel": [2] * 3, "stokes_reg_vel_omega": [2] * 3 + [4] * 3}[kernel]
+             "stokes_reg_vel": [2] * 3, "stokes_reg_vel_omega": [2] * 3 + [4] * 3,
+             "laplace_pgradgrad": [2] + [4] * 3 + [8] * 6,
+             "laplace_qpgradgrad": [2] + [4] * 3 + [8] * 6}[kernel]
     np.testing.assert_allclose(b, a * np.array(scale, float), rtol=0, atol=1e-13 * np.abs(b).max())
 
 

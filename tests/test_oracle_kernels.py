@@ -273,3 +273,74 @@ def test_reg_vel_omega_mobility_is_symmetric():
         for a in range(2):
             Mb[6 * a:6 * a + 6, j] = sum(pair_values("G_eps+Omega+T+W", x[a] - x[b], s[b]) for b in range(2))
     np.testing.assert_allclose(Mb, Mb.T, rtol=0, atol=1e-14)
+
+
+# ---- LapPGradGrad, Table III ------------------------------
+def test_pgradgrad_derivatives_and_harmonicity():
+    rng = np.random.default_rng(31)
+    h = 1e-5
+    for _ in range(4):
+        r = rng.standard_normal(3)
+        s = rng.standard_normal(4)
+        v = pair_values("LD+gradLD+gradgradLD", r, s)
+        # grad phi and grad grad phi are the target derivatives of phi and grad phi
+        for k in range(3):
+            e = np.zeros(3)
+            e[k] = h
+            dv = (pair_values("LD+gradLD+gradgradLD", r + e, s) - pair_values("LD+gradLD+gradgradLD", r - e, s)) / (2 * h)
+            np.testing.assert_allclose(dv[0], v[1 + k], rtol=1e-7, atol=1e-9)
+            H = {(0, 0): 4, (0, 1): 5, (0, 2): 6, (1, 1): 7, (1, 2): 8, (2, 2): 9}
+            for j in range(3):
+                np.testing.assert_allclose(dv[1 + j], v[H[tuple(sorted((j, k)))]], rtol=1e-6, atol=1e-8)
+        # phi is harmonic away from the source: trace of grad grad phi = 0
+        assert abs(v[4] + v[7] + v[9]) < 1e-12 * np.abs(v[4:]).max()
+
+
+def test_dipole_is_limit_of_charge_pair():
+    # L^D_j = -dL/dx_j: a dipole d at y is the limit of charges +1/h at
+    # y + h d / 2 and -1/h at y - h d / 2
+    rng = np.random.default_rng(32)
+    r = rng.standard_normal(3)
+    d = rng.standard_normal(3)
+    h = 1e-5
+    pair = (pair_values("L+gradL+gradgradL", r - 0.5 * h * d, np.array([1.0]))
+            - pair_values("L+gradL+gradgradL", r + 0.5 * h * d, np.array([1.0]))) / h
+    dip = pair_values("LD+gradLD+gradgradLD", r, np.concatenate([[0.0], d]))
+    np.testing.assert_allclose(dip, pair, rtol=1e-5, atol=1e-7)
+    # charges only: the S->T kernel reduces to the T-column kernel, and the S row to L + L^D's phi
+    q = np.array([1.7, 0, 0, 0])
+    np.testing.assert_allclose(pair_values("LD+gradLD+gradgradLD", r, q), pair_values("L+gradL+gradgradL", r, q[:1]),
+                               rtol=1e-15)
+    sd = np.concatenate([[0.3], d])
+    np.testing.assert_allclose(pair_values("L+LD", r, sd), pair_values("LD+gradLD+gradgradLD", r, sd)[:1], rtol=1e-15)
+    # worked value: dipole d = (0, 0, 4 pi) at r = (0, 0, 2): phi = d.r/(4 pi r^3) = 1/4
+    np.testing.assert_allclose(pair_values("L+LD", np.array([0, 0, 2.0]), np.array([0, 0, 0, 4 * np.pi])), [0.25])
+
+
+# ---- LapQPGradGrad (Table XI; L^Q_jk = d2 L / dx_j dx_k) ----
+def test_qpgradgrad_derivatives_and_limits():
+    rng = np.random.default_rng(41)
+    h = 1e-5
+    H = {(0, 0): 4, (0, 1): 5, (0, 2): 6, (1, 1): 7, (1, 2): 8, (2, 2): 9}
+    for _ in range(4):
+        r = rng.standard_normal(3) + 0.5
+        Q = rng.standard_normal(9)
+        v = pair_values("LQ+gradLQ+gradgradLQ", r, Q)
+        np.testing.assert_allclose(pair_values("LQ", r, Q), v[:1], rtol=1e-15)
+        for k in range(3):
+            e = np.zeros(3)
+            e[k] = h
+            dv = (pair_values("LQ+gradLQ+gradgradLQ", r + e, Q) - pair_values("LQ+gradLQ+gradgradLQ", r - e, Q)) / (2 * h)
+            np.testing.assert_allclose(dv[0], v[1 + k], rtol=1e-6, atol=1e-8)
+            for j in range(3):
+                np.testing.assert_allclose(dv[1 + j], v[H[tuple(sorted((j, k)))]], rtol=1e-6, atol=1e-8)
+        assert abs(v[4] + v[7] + v[9]) < 1e-11 * np.abs(v[4:]).max()  # harmonic
+        # the quadrupole Q = a b^T is the limit of dipoles +b/h at y + h a/2 and -b/h at
+        # y - h a/2 (r = x - y, so the first sits at r - h a/2)
+        a, b = rng.standard_normal(3), rng.standard_normal(3)
+        lim = (pair_values("LD+gradLD+gradgradLD", r - 0.5 * h * a, np.concatenate([[0.0], b]))
+               - pair_values("LD+gradLD+gradgradLD", r + 0.5 * h * a, np.concatenate([[0.0], b]))) / h
+        np.testing.assert_allclose(pair_values("LQ+gradLQ+gradgradLQ", r, np.outer(a, b).ravel()), lim,
+                                   rtol=1e-5, atol=1e-7)
+    # an isotropic Q = I has phi = tr(d d L) = lap L = 0 away from the source
+    assert abs(pair_values("LQ", np.array([0.3, -0.2, 0.7]), np.eye(3).ravel())[0]) < 1e-14

@@ -26,6 +26,10 @@ Recipe:
           b (C6, RPY [f, b] -> [u, lap u]) or eps (C7, StokesRegVelOmega
           [f, t, eps] -> [u, omega], Table VI) iid U[0, 1e-4] in the paper's units
           (PAPER.md:676), i.e. U[0, 1e-4 / 32] in the unit cube; p = 10
+  C8      the same cloud and values for LapPGradGrad [q, d] -> [phi, grad phi,
+          grad grad phi] (Table III; the paper's Fig. 3a case)
+  C9      the same for LapQPGradGrad Q -> [phi, grad phi, grad grad phi]
+          (Table XI; the paper's Fig. 3b case)
 The BASELINE configs are the paper-shaped stand-ins for the paper's own
 synthetic clouds (Eq. (ptdist)); no dataset is involved.
 """
@@ -36,12 +40,14 @@ import numpy as np
 
 SEED_ROOT = 201015155
 
-KERNELS = ("laplace_pgrad", "stokeslet", "rpy", "stokes_reg_vel", "stokes_reg_vel_omega")
+KERNELS = ("laplace_pgrad", "stokeslet", "rpy", "stokes_reg_vel", "stokes_reg_vel_omega", "laplace_pgradgrad",
+           "laplace_qpgradgrad")
 # (k_s, k_t) per kernel: PAPER.md Table XI (lines 874-880)
 KERNEL_DIMS = {"laplace_pgrad": (1, 4), "stokeslet": (3, 3), "rpy": (4, 6), "stokes_reg_vel": (4, 3),
-               "stokes_reg_vel_omega": (7, 6)}
+               "stokes_reg_vel_omega": (7, 6), "laplace_pgradgrad": (4, 10), "laplace_qpgradgrad": (9, 10)}
 # C-ABI enum values (include/kafmm.h)
-KERNEL_ENUM = {"laplace_pgrad": 1, "stokeslet": 2, "rpy": 3, "stokes_reg_vel": 4, "stokes_reg_vel_omega": 5}
+KERNEL_ENUM = {"laplace_pgrad": 1, "stokeslet": 2, "rpy": 3, "stokes_reg_vel": 4, "stokes_reg_vel_omega": 5,
+               "laplace_pgradgrad": 6, "laplace_qpgradgrad": 7}
 # source column of the nonlinear per-source parameter (b or eps), if any
 PARAM_COL = {"rpy": 3, "stokes_reg_vel": 3, "stokes_reg_vel_omega": 6}
 
@@ -70,6 +76,8 @@ CONFIGS = {
     5: ConfigSpec(5, "stokeslet", 64_000_000, 8, 128, "spheres"),
     6: ConfigSpec(6, "rpy", 1_000_000, 10, 2000, "lognormal", 1e-4 / 32, True),
     7: ConfigSpec(7, "stokes_reg_vel_omega", 1_000_000, 10, 2000, "lognormal", 1e-4 / 32, True),
+    8: ConfigSpec(8, "laplace_pgradgrad", 1_000_000, 10, 2000, "lognormal", 0.0, True),
+    9: ConfigSpec(9, "laplace_qpgradgrad", 1_000_000, 10, 2000, "lognormal", 0.0, True),
 }
 LOGNORMAL_M, LOGNORMAL_S = -1.0, 0.5
 
@@ -168,7 +176,8 @@ def make_values(spec: ConfigSpec, n: int | None = None):
     k_s = KERNEL_DIMS[spec.kernel][0]
     if spec.poly:
         vals = rv.uniform(-1.0, 1.0, size=(n, k_s))
-        vals[:, PARAM_COL[spec.kernel]] = rv.uniform(0.0, spec.extra, size=n)
+        if spec.kernel in PARAM_COL:
+            vals[:, PARAM_COL[spec.kernel]] = rv.uniform(0.0, spec.extra, size=n)
     elif spec.kernel == "laplace_pgrad":
         vals = rv.standard_normal((n, 1))
     elif spec.kernel == "stokeslet":
