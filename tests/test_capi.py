@@ -43,8 +43,13 @@ def test_kernel_dims_and_status_strings(lib):
     assert kernel_dims("stokeslet") == (3, 3)
     assert kernel_dims("rpy") == (4, 6)
     assert kernel_dims("stokes_reg_vel") == (4, 3)
+    assert kernel_dims("stokes_reg_vel_omega") == (7, 6)    # Table XI StokesRegVelOmega
+    assert kernel_dims("laplace_pgradgrad") == (4, 10)      # LapPGradGrad, SL + DL at every point
+    assert kernel_dims("laplace_qpgradgrad") == (9, 10)     # LapQPGradGrad
     with pytest.raises(KafmmError):
-        kernel_dims(7)
+        kernel_dims(8)
+    with pytest.raises(KafmmError):
+        kernel_dims(0)
     assert lib.kafmm_status_string(2) == b"point outside [0,1)^3"
     assert lib.kafmm_stage_name(4) == b"m2l"
 
