@@ -215,6 +215,22 @@ kafmm_status kafmm_gather_rows(kafmm_plan plan, const double* src, int ld, const
 kafmm_status kafmm_scatter_rows(kafmm_plan plan, const double* src, int ld, const int64_t* idx, int64_t n,
                                 double* dst);
 
+/* ---- RPY above a no-slip wall (Table X) ----
+ * Particles in [0,1) x [0,1) x (1/2, 1) above the wall plane z = 1/2 (device,
+ * n x 3); the library adds their mirror images (z -> 1 - z) and runs four
+ * KAFMM summations over the 2n points (RPY, LapPGradGrad twice,
+ * LapQPGradGrad), then assembles per particle
+ *   u = u^S + grad phi^SDZ + x3 (grad phi^SD + grad phi^Q) - [0, 0, phi^SD + phi^Q],
+ *   lap u = lap u^S + 2 d/dx3 grad (phi^SD + phi^Q),   x3 = z - 1/2.
+ * src_values: device n x 4 [f, b]; trg_out: device n x 6 [u, lap u], user order.
+ * EDOMAIN if a particle is not strictly above the wall.  The quadrupole sum
+ * sits at the image points (reading R18). */
+typedef struct kafmm_wall_s* kafmm_wall;
+kafmm_status kafmm_wall_setup(const double* points, int64_t n, int p, int max_pts_per_leaf, kafmm_wall* out);
+kafmm_status kafmm_wall_set_stream(kafmm_wall w, void* stream);
+kafmm_status kafmm_wall_eval(kafmm_wall w, const double* src_values, double* trg_out);
+void kafmm_wall_destroy(kafmm_wall w);
+
 #ifdef __cplusplus
 }
 #endif

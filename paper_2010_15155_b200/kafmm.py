@@ -71,6 +71,10 @@ _SIGS = [
     ("kafmm_unpack_ue", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("kafmm_gather_rows", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
     ("kafmm_scatter_rows", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("kafmm_wall_setup", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("kafmm_wall_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kafmm_wall_eval", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("kafmm_wall_destroy", None, [C.c_void_p]),
 ]
 EXPORTED = [s[0] for s in _SIGS]
 
@@ -267,3 +271,44 @@ class KAFMM:
         n = C.c_int()
         _check(self.lib.kafmm_launch_count(self.h, C.byref(n)), "kafmm_launch_count")
         return n.value
+
+
+class KAFMMWall:
+    """RPY spheres above a no-slip wall (Table X): particles in
+    [0,1)^2 x (1/2, 1), wall at z = 1/2.  eval([f, b]) -> [u, lap u]."""
+
+    def __init__(self, points, p: int, max_pts: int, stream=None):
+        torch = _torch()
+        self.lib = load_library()
+        if isinstance(points, np.ndarray):
+            pts = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float64)).cuda()
+        else:
+            pts = points.to(device="cuda", dtype=torch.float64).contiguous()
+        self.n = int(pts.shape[0])
+        h = C.c_void_p()
+        torch.cuda.synchronize()
+        _check(self.lib.kafmm_wall_setup(C.c_void_p(pts.data_ptr()), self.n, int(p), int(max_pts), C.byref(h)),
+               "kafmm_wall_setup")
+        self.h = h
+        if stream is not None:
+            ptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+            _check(self.lib.kafmm_wall_set_stream(self.h, C.c_void_p(ptr)), "kafmm_wall_set_stream")
+
+    def eval(self, src, out=None):
+        torch = _torch()
+        assert src.is_cuda and src.dtype == torch.float64 and src.shape == (self.n, 4)
+        src = src.contiguous()
+        if out is None:
+            out = torch.empty((self.n, 6), dtype=torch.float64, device=src.device)
+        _check(self.lib.kafmm_wall_eval(self.h, C.c_void_p(src.data_ptr()), C.c_void_p(out.data_ptr())),
+               "kafmm_wall_eval")
+        return out
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            self.lib.kafmm_wall_destroy(h)
+            self.h = None
+
+    def close(self):
+        self.__del__()
