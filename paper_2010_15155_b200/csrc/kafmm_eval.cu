@@ -70,8 +70,8 @@ __device__ __forceinline__ void copy_records(double* __restrict__ ss, int fill, 
 // jobs[j] = target box; sources = the box's own points (roff == nullptr, S2M)
 // or the merged point ranges rng[roff[j] .. roff[j+1]) of its X list (S2L).
 // TQ check points per thread (TQ * PT_THREADS >= M).
-template <class K, int SREC, int TQ, bool ADD>
-__global__ void __launch_bounds__(PT_THREADS)
+template <class K, int SREC, int TQ, bool ADD, int NTH>
+__global__ void __launch_bounds__(NTH)
     k_points_to_surface(const int32_t* __restrict__ jobs, const int64_t* __restrict__ roff,
                         const int2* __restrict__ rng, const int32_t* __restrict__ level,
                         const int32_t* __restrict__ ijk, const int64_t* __restrict__ pbeg,
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(PT_THREADS)
   double tx[TQ], ty[TQ], tz[TQ], acc[TQ][K::KT];
 #pragma unroll
   for (int q = 0; q < TQ; ++q) {
-    int i = min(tid + PT_THREADS * q, M - 1);
+    int i = min(tid + NTH * q, M - 1);
     tx[q] = cx + sc * surf[3 * i];
     ty[q] = cy + sc * surf[3 * i + 1];
     tz[q] = cz + sc * surf[3 * i + 2];
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(PT_THREADS)
   double* o = out + (int64_t)b * ldn;
 #pragma unroll
   for (int q = 0; q < TQ; ++q) {
-    int i = tid + PT_THREADS * q;
+    int i = tid + NTH * q;
     if (i < M) {
 #pragma unroll
       for (int a = 0; a < K::KT; ++a) {
@@ -191,12 +191,23 @@ __device__ __forceinline__ void tile_reduce_store(const Tile<TP>& z, double (&ac
   }
 }
 
-// pair loop over a chunk of cnt staged sources (SSTR doubles each)
+// pair loop over a chunk of cnt staged sources (SSTR doubles each); with one
+// target per thread two interleaved accumulator sets give independent chains
 template <class K, int SSTR, int TP>
 __device__ __forceinline__ void tile_pairs(const Tile<TP>& z, const double* ss, int cnt, const double (&tx)[TP],
-                                           const double (&ty)[TP], const double (&tz)[TP], double (&acc)[TP][K::KT]) {
+                                           const double (&ty)[TP], const double (&tz)[TP], double (&acc)[TP][K::KT],
+                                           double (&acc2)[K::KT]) {
   if (!z.act) return;
-  for (int j = z.sl; j < cnt; j += z.S) {
+  int j = z.sl;
+  if (TP == 1) {
+    for (; j + z.S < cnt; j += 2 * z.S) {
+      const double* sr = ss + j * SSTR;
+      const double* s2 = sr + z.S * SSTR;
+      K::acc(tx[0] - sr[0], ty[0] - sr[1], tz[0] - sr[2], sr + 3, acc[0]);
+      K::acc(tx[0] - s2[0], ty[0] - s2[1], tz[0] - s2[2], s2 + 3, acc2);
+    }
+  }
+  for (; j < cnt; j += z.S) {
     const double* sr = ss + j * SSTR;
     const double sx = sr[0], sy = sr[1], sz = sr[2];
 #pragma unroll
@@ -207,7 +218,7 @@ __device__ __forceinline__ void tile_pairs(const Tile<TP>& z, const double* ss, 
 // a9 + a10: L2T (own downward equivalent, level >= 2) and M2T (W list) ------
 // Sources are generated surface points (lattice offset x radius + centre) with
 // their equivalent densities; SSTR doubles per source in the chunk.
-template <class K, int SSTR>
+template <class K, int SSTR, int TP>
 __global__ void __launch_bounds__(PT_THREADS)
     k_leaf_far(const int32_t* __restrict__ leaves, const int32_t* __restrict__ level, const int32_t* __restrict__ ijk,
                const int64_t* __restrict__ pbeg, const int64_t* __restrict__ pend, const double* __restrict__ pts,
@@ -221,10 +232,11 @@ __global__ void __launch_bounds__(PT_THREADS)
   const int64_t p0 = pbeg[b], p1 = pend[b];
   const int lb = level[b];
   const int64_t e0 = w_off[job], e1 = w_off[job + 1];
-  constexpr int TP = TPof<K>::v;
   for (int64_t t0 = p0; t0 < p1; t0 += TP * PT_THREADS) {
     Tile<TP> z((int)min((int64_t)TP * PT_THREADS, p1 - t0));
-    double tx[TP], ty[TP], tz[TP], acc[TP][K::KT];
+    double tx[TP], ty[TP], tz[TP], acc[TP][K::KT], acc2[K::KT];
+#pragma unroll
+    for (int a = 0; a < K::KT; ++a) acc2[a] = 0.0;
 #pragma unroll
     for (int i = 0; i < TP; ++i) {
       const int64_t ti = t0 + min(i * z.NTT + z.tt, z.nt - 1);
@@ -236,7 +248,7 @@ __global__ void __launch_bounds__(PT_THREADS)
     }
     auto run = [&](int cnt) {
       __syncthreads();
-      tile_pairs<K, SSTR, TP>(z, ss, cnt, tx, ty, tz, acc);
+      tile_pairs<K, SSTR, TP>(z, ss, cnt, tx, ty, tz, acc, acc2);
       __syncthreads();
     };
     int fill = 0;
@@ -267,12 +279,14 @@ __global__ void __launch_bounds__(PT_THREADS)
       }
     }
     if (fill) run(fill);
+#pragma unroll
+    for (int a = 0; a < K::KT; ++a) acc[0][a] += acc2[a];
     tile_reduce_store<TP, K::KT>(z, acc, ss, outs + t0 * K::KT, false);
   }
 }
 
 // a11: P2P over the U list: merged source ranges streamed through shared memory
-template <class K, int SREC>
+template <class K, int SREC, int TP>
 __global__ void __launch_bounds__(PT_THREADS)
     k_p2p(const int32_t* __restrict__ leaves, const int64_t* __restrict__ pbeg, const int64_t* __restrict__ pend,
           const double* __restrict__ rec, const int64_t* __restrict__ roff, const int2* __restrict__ rng,
@@ -283,10 +297,11 @@ __global__ void __launch_bounds__(PT_THREADS)
   const int b = leaves[job];
   const int64_t p0 = pbeg[b], p1 = pend[b];
   const int64_t r0 = roff[job], r1 = roff[job + 1];
-  constexpr int TP = TPof<K>::v;
   for (int64_t t0 = p0; t0 < p1; t0 += TP * PT_THREADS) {
     Tile<TP> z((int)min((int64_t)TP * PT_THREADS, p1 - t0));
-    double tx[TP], ty[TP], tz[TP], acc[TP][K::KT];
+    double tx[TP], ty[TP], tz[TP], acc[TP][K::KT], acc2[K::KT];
+#pragma unroll
+    for (int a = 0; a < K::KT; ++a) acc2[a] = 0.0;
 #pragma unroll
     for (int i = 0; i < TP; ++i) {
       const int64_t ti = t0 + min(i * z.NTT + z.tt, z.nt - 1);
@@ -298,7 +313,7 @@ __global__ void __launch_bounds__(PT_THREADS)
     }
     auto run = [&](int cnt) {
       __syncthreads();
-      tile_pairs<K, SREC, TP>(z, ss, cnt, tx, ty, tz, acc);
+      tile_pairs<K, SREC, TP>(z, ss, cnt, tx, ty, tz, acc, acc2);
       __syncthreads();
     };
     int fill = 0;
@@ -318,6 +333,8 @@ __global__ void __launch_bounds__(PT_THREADS)
       }
     }
     if (fill) run(fill);
+#pragma unroll
+    for (int a = 0; a < K::KT; ++a) acc[0][a] += acc2[a];
     tile_reduce_store<TP, K::KT>(z, acc, ss, outs + t0 * K::KT, true);
   }
 }
@@ -344,20 +361,22 @@ __global__ void k_check_values(const double* __restrict__ v, int64_t n, int ks, 
 // ---------------------------------------------------------------------------
 static inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
-// S2M / S2L launch with TQ = ceil(M / PT_THREADS) check points per thread
+// S2M / S2L launch: NTH threads x TQ check points per thread >= M, chosen so
+// few slots idle (p = 8: 64 x 5 = 320 for 296; p = 10: 128 x 4; p = 12: 128 x 6)
 template <class K, int SREC, bool ADD>
 static void launch_surface(Plan& P, const int32_t* jobs, int64_t njobs, const int64_t* roff, const int2* rng,
                            double alpha) {
-  const int tq = (P.M + PT_THREADS - 1) / PT_THREADS;
-#define KF_SURF(TQ)                                                                                          \
-  k_points_to_surface<K, SREC, TQ, ADD><<<(unsigned)njobs, PT_THREADS, 0, P.stream>>>(                     \
+#define KF_SURF(TQ, NTH)                                                                                     \
+  k_points_to_surface<K, SREC, TQ, ADD, NTH><<<(unsigned)njobs, NTH, 0, P.stream>>>(                       \
       jobs, roff, rng, P.d_level, P.d_ijk, P.d_pbeg, P.d_pend, P.d_rec, P.d_surf, P.M, alpha, P.d_chk, P.ldn)
-  if (tq <= 1) KF_SURF(1);
-  else if (tq == 2) KF_SURF(2);
-  else if (tq == 3) KF_SURF(3);
-  else if (tq == 4) KF_SURF(4);
-  else if (tq <= 6) KF_SURF(6);
-  else if (tq <= 8) KF_SURF(8);
+  const int M = P.M;
+  if (M <= 128) KF_SURF(1, 128);
+  else if (M <= 256) KF_SURF(2, 128);
+  else if (M <= 320) KF_SURF(5, 64);
+  else if (M <= 384) KF_SURF(3, 128);
+  else if (M <= 512) KF_SURF(4, 128);
+  else if (M <= 768) KF_SURF(6, 128);
+  else if (M <= 1024) KF_SURF(8, 128);
   else throw Error{KAFMM_EINVAL, "p too large for the surface kernels (M > 1024)"};
 #undef KF_SURF
   KF_CHECK_LAUNCH();
@@ -416,17 +435,29 @@ static void eval_down_impl(Plan& P, double* d_out) {
   }
   mark(ST_L2L);  // L2L is interleaved with DC2DE per level; its own slot stays empty
   mark(ST_LEAF_FAR);
+  // TP targets per thread pays off for leaves of >= 48 points (C5-like); small
+  // leaves keep one target per thread and more source slices
+  const bool big = P.nleaf > 0 && P.n >= 48 * P.nleaf;
+  constexpr int TPT = TPof<KT_>::v, TPS = TPof<KST>::v, SST = (3 + KT_::KS + 1) / 2 * 2;
   if (J.nleaf > 0) {
-    k_leaf_far<KT_, (3 + KT_::KS + 1) / 2 * 2><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(
-        J.leaf_ids, P.d_level, P.d_ijk, P.d_pbeg, P.d_pend, P.d_pts, J.w_off, J.w_src, P.d_ue, P.d_de, P.ldn,
-        P.d_surf, P.M, P.d_outs);
+#define KF_FAR(TP)                                                                                             \
+  k_leaf_far<KT_, SST, TP><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(J.leaf_ids, P.d_level, P.d_ijk, P.d_pbeg,  \
+                                                                    P.d_pend, P.d_pts, J.w_off, J.w_src, P.d_ue, \
+                                                                    P.d_de, P.ldn, P.d_surf, P.M, P.d_outs)
+    if (big) KF_FAR(TPT);
+    else KF_FAR(1);
+#undef KF_FAR
     KF_CHECK_LAUNCH();
     P.launches++;
   }
   mark(ST_P2P);
   if (J.nleaf > 0) {
-    k_p2p<KST, SREC><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(J.leaf_ids, P.d_pbeg, P.d_pend, P.d_rec, J.u_roff,
-                                                               J.u_rng, P.d_outs);
+    if (big)
+      k_p2p<KST, SREC, TPS><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(J.leaf_ids, P.d_pbeg, P.d_pend, P.d_rec,
+                                                                      J.u_roff, J.u_rng, P.d_outs);
+    else
+      k_p2p<KST, SREC, 1><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(J.leaf_ids, P.d_pbeg, P.d_pend, P.d_rec,
+                                                                    J.u_roff, J.u_rng, P.d_outs);
     KF_CHECK_LAUNCH();
     P.launches++;
   }

@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -553,15 +554,24 @@ void run_m2l_fft(Plan& Pl) {
         k_m2l_pairs<3><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
                                                              Pl.d_cb, ch.d_tpb, ch.d_pl_off, ch.d_pl);
     } else {
-      const int ppc = DM_WARPS * 8 * (Pl.kml == 1 ? NT_L : NT_G);
+      // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
+      // (fewer registers, more resident warps) -- a tuning knob measured in profiles/
+      static const bool half = getenv("KAFMM_DMMA_NT") != nullptr;
+      const int nt = (Pl.kml == 1 ? NT_L : NT_G) / (half ? 2 : 1);
+      const int ppc = DM_WARPS * 8 * nt;
       const int npb = (int)((ch.npar + ppc - 1) / ppc);
       const unsigned grid = (unsigned)((int64_t)npb * Pl.NF);
-      if (Pl.kml == 1)
-        k_m2l_dmma<1, NT_L><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb,
-                                                                   ch.d_nbr, Pl.d_aidx);
-      else
-        k_m2l_dmma<3, NT_G><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb,
-                                                                   ch.d_nbr, Pl.d_aidx);
+#define KF_DMMA(KML, NT)                                                                                        \
+  k_m2l_dmma<KML, NT><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb, \
+                                                             ch.d_nbr, Pl.d_aidx)
+      if (Pl.kml == 1) {
+        if (half) KF_DMMA(1, NT_L / 2);
+        else KF_DMMA(1, NT_L);
+      } else {
+        if (half) KF_DMMA(3, NT_G / 2);
+        else KF_DMMA(3, NT_G);
+      }
+#undef KF_DMMA
     }
     KF_CHECK_LAUNCH();
     prod_mark(Pl);
