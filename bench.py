@@ -361,6 +361,7 @@ def main():
                 "frac": p2p_flop / (p2p_ms * 1e-3) / 1e12 / peak_dfma, "pairs": n_p2p_local,
                 "flop_per_pair": P2P_FLOPS[spec.kernel], "ms": p2p_ms},
         "stages_ms": stage_mean,
+        "fft_m2l": plan.fft_stats() if mode.startswith("fft") else None,
         "clocks": clocks,
         "gpu_launches": launches,
         "e2e": e2e,

@@ -176,6 +176,12 @@ const char* kafmm_stage_name(int stage);
 kafmm_status kafmm_set_m2l_mode(kafmm_plan plan, int mode);
 kafmm_status kafmm_get_m2l_mode(kafmm_plan plan, int* mode);
 
+/* FFT M2L work summary, st[8]: chunks, source parent blocks (incl. halos
+ * transformed once per chunk), target parents, target boxes, V pairs, chunks
+ * whose product runs per pair under the current mode, frequency bins NF,
+ * spectra budget in bytes. */
+kafmm_status kafmm_fft_stats(kafmm_plan plan, int64_t* st);
+
 /* Kernel launches issued by one kafmm_eval. */
 kafmm_status kafmm_launch_count(kafmm_plan plan, int* n);
 

@@ -119,12 +119,14 @@ kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int
   {
     size_t fr = 0, tot = 0;
     KF_CUDA(cudaMemGetInfo(&fr, &tot));
-    int64_t budget = std::min<int64_t>((int64_t)16 << 30, (int64_t)(fr / 4));
+    // spectra budget of the FFT M2L chunks: larger chunks transform fewer halo boxes twice
+    int64_t budget = std::min<int64_t>((int64_t)40 << 30, (int64_t)(fr / 3));
     const char* env = getenv("KAFMM_FFT_BUDGET_MB");
     if (env) budget = (int64_t)atoll(env) << 20;
     build_fft_m2l(*P, budget);
     const char* m = getenv("KAFMM_M2L");
     if (m && std::string(m) == "dense") P->m2l_mode = M2L_DENSE;
+    if (P->m2l_mode == M2L_DENSE) build_dense_m2l(*P);
   }
   P->d_rec = dalloc<double>(*P, (size_t)n * P->srec);
   P->d_outs = dalloc<double>(*P, (size_t)n * kt);
@@ -337,8 +339,11 @@ kafmm_status kafmm_set_m2l_mode(kafmm_plan plan, int mode) {
     set_error("FFT M2L not available for this p");
     return KAFMM_EINVAL;
   }
+  KF_API_BEGIN
+  if (mode == M2L_DENSE) build_dense_m2l(*plan);
   plan->m2l_mode = mode;
   return KAFMM_OK;
+  KF_API_END
 }
 
 kafmm_status kafmm_get_m2l_mode(kafmm_plan plan, int* mode) {
@@ -410,6 +415,22 @@ kafmm_status kafmm_scatter_rows(kafmm_plan plan, const double* src, int ld, cons
   scatter_rows(*plan, src, ld, idx, n, dst);
   return KAFMM_OK;
   KF_API_END
+}
+
+kafmm_status kafmm_fft_stats(kafmm_plan plan, int64_t* st) {
+  if (!plan || !st) return KAFMM_EINVAL;
+  for (int i = 0; i < 8; ++i) st[i] = 0;
+  for (const FftChunk& ch : plan->fft_chunks) {
+    st[0] += 1;
+    st[1] += ch.nq;
+    st[2] += ch.npar;
+    st[3] += ch.nt;
+    st[4] += ch.npairs;
+    st[5] += (plan->m2l_mode == M2L_FFT_PAIRS || (plan->m2l_mode == M2L_FFT && ch.block_fill < FFT_PAIR_FILL)) ? 1 : 0;
+  }
+  st[6] = plan->NF;
+  st[7] = plan->fft_budget;
+  return KAFMM_OK;
 }
 
 kafmm_status kafmm_launch_count(kafmm_plan plan, int* n) {

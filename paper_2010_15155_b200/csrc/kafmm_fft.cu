@@ -536,7 +536,7 @@ static void launch_inv(Plan& Pl, const FftChunk& ch) {
 
 bool fft_supported_p(int p) { return (p >= 3 && p <= 8) || p == 10 || p == 12; }
 
-constexpr int NT_L = 8, NT_G = 4;  // parent n-tiles per warp (Laplace, Stokes family)
+constexpr int NT_L = 4, NT_G = 2;  // parent n-tiles per warp (Laplace, Stokes family); measured best (profiles/)
 
 void run_m2l_fft(Plan& Pl) {
   for (const FftChunk& ch : Pl.fft_chunks) {

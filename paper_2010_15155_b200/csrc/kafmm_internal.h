@@ -252,6 +252,7 @@ inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
 // translation units
 void build_tree_and_lists(Plan& P, const double* d_points);   // kafmm_tree.cu
 void build_operators(Plan& P);                               // kafmm_ops.cu
+void build_dense_m2l(Plan& P);                               // kafmm_ops.cu (lazy)
 void build_gemm_batches(Plan& P);                            // kafmm_tree.cu
 void upload_batch(Plan& P, GemmBatch& g, const std::vector<int2>& h_items);
 void run_eval(Plan& P, const double* d_src, double* d_out);  // kafmm_eval.cu

@@ -188,16 +188,6 @@ void build_operators(Plan& P) {
   }
   KF_CUDA(cudaStreamSynchronize(st));
   cublasDestroy(bh);
-  // raw M2L matrices for the 316 offsets (same enumeration as the list builder)
-  P.d_m2l = dalloc<double>(P, (size_t)N_OFFSETS * P.op_stride);
-  int id = 0;
-  for (int a = 0; a < 343; ++a) {
-    int ox = a / 49 - 3, oy = (a / 7) % 7 - 3, oz = a % 7 - 3;
-    if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) < 2) continue;
-    double cs[3] = {c0[0] + 2.0 * h0 * ox, c0[1] + 2.0 * h0 * oy, c0[2] + 2.0 * h0 * oz};
-    fill(P, P.d_m2l + (size_t)id * P.op_stride, P.ldn, c0, ALPHA_DC * h0, cs, ALPHA_UE * h0);
-    ++id;
-  }
   KF_CUDA(cudaFreeAsync(K, st));
   KF_CUDA(cudaFreeAsync(UA, st));
   KF_CUDA(cudaFreeAsync(VTA, st));
@@ -207,6 +197,23 @@ void build_operators(Plan& P) {
   KF_CUDA(cudaFreeAsync(tmp, st));
   KF_CUDA(cudaFreeAsync(Kp, st));
   KF_CUDA(cudaStreamSynchronize(st));
+}
+
+// raw M2L matrices for the 316 offsets (same enumeration as the list builder),
+// only for the dense M2L variant: built on first use (C4: 12.5 GB)
+void build_dense_m2l(Plan& P) {
+  if (P.d_m2l) return;
+  const double h0 = 0.5, c0[3] = {0.5, 0.5, 0.5};
+  P.d_m2l = dalloc<double>(P, (size_t)N_OFFSETS * P.op_stride);
+  int id = 0;
+  for (int a = 0; a < 343; ++a) {
+    int ox = a / 49 - 3, oy = (a / 7) % 7 - 3, oz = a % 7 - 3;
+    if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) < 2) continue;
+    double cs[3] = {c0[0] + 2.0 * h0 * ox, c0[1] + 2.0 * h0 * oy, c0[2] + 2.0 * h0 * oz};
+    fill(P, P.d_m2l + (size_t)id * P.op_stride, P.ldn, c0, ALPHA_DC * h0, cs, ALPHA_UE * h0);
+    ++id;
+  }
+  KF_CUDA(cudaStreamSynchronize(P.stream));
 }
 
 }  // namespace kafmm

@@ -64,6 +64,7 @@ _SIGS = [
     ("kafmm_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     ("kafmm_set_m2l_mode", C.c_int, [C.c_void_p, C.c_int]),
     ("kafmm_get_m2l_mode", C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+    ("kafmm_fft_stats", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kafmm_restrict", C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
     ("kafmm_eval_up", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kafmm_eval_down", C.c_int, [C.c_void_p, C.c_void_p]),
@@ -266,6 +267,13 @@ class KAFMM:
         _check(self.lib.kafmm_scatter_rows(self.h, C.c_void_p(src.data_ptr()), int(dst.shape[1]),
                                            C.c_void_p(idx.data_ptr()), int(idx.numel()), C.c_void_p(dst.data_ptr())),
                "kafmm_scatter_rows")
+
+    def fft_stats(self) -> dict:
+        st = np.zeros(8, np.int64)
+        _check(self.lib.kafmm_fft_stats(self.h, C.c_void_p(st.ctypes.data)), "kafmm_fft_stats")
+        keys = ("chunks", "source_blocks", "target_parents", "targets", "v_pairs", "pair_chunks", "n_freq",
+                "budget_bytes")
+        return {k: int(v) for k, v in zip(keys, st)}
 
     def launch_count(self) -> int:
         n = C.c_int()

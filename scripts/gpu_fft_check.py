@@ -42,6 +42,7 @@ for cid in [int(a) for a in sys.argv[1:] if a.isdigit()]:
     torch.cuda.synchronize()
     ts = time.time() - t
     src = torch.from_numpy(vals).cuda()
+    print(f"C{cid} fft stats", plan.fft_stats(), flush=True)
     res = {}
     for mode in MODES:
         if mode == "dense" and cid >= 3:
