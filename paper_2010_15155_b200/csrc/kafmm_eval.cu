@@ -189,6 +189,7 @@ __device__ __forceinline__ void tile_reduce_store(const Tile<TP>& z, double (&ac
       }
     }
   }
+  __syncthreads();  // red aliases the source chunk the next pass refills
 }
 
 // pair loop over a chunk of cnt staged sources (SSTR doubles each); with one

@@ -100,30 +100,90 @@ __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
   acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
 }
 
-// The DFT passes below are direct sums over the p lattice points (or NG grid
-// frequencies) of one line.  Each thread produces FT outputs of one line from
-// a single read of every input value; the FT twiddles w^(f i) it needs at a
-// step are the same for every lane of the warp (lanes run over lines), so
-// their shared-memory reads are broadcasts.
-constexpr int FT = 5;
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// The DFT passes run as small real GEMMs on the FP64 tensor cores: a pass maps
+// the NIN inputs of every line to NOUT complex outputs,
+//     out[line][o] = sum_i in[line][i] w^(s o i),  w = exp(2 pi i / NG),
+// written as C[line][(o, re|im)] = sum_(i, re|im) A[line][(i, re|im)] B[(i, .)][(o, .)]
+// with B the 2x2 real blocks of the twiddles (1x2 for a real input).  Lines
+// are the M dimension (8 per DMMA), the twiddle matrix B sits in registers for
+// the whole pass (one table per pass shape, built at setup), and a lane's C
+// fragment holds the (re, im) pair of one output, stored as one 16-B word.
+template <int P>
+struct DftShape {
+  static constexpr int NG = 2 * P - 1, NZ = NG / 2 + 1;
+  // forward z (real in: P -> NZ), forward y / x (complex: P -> NG), inverse x / y (complex: NG -> P)
+  static constexpr int KZ = (P + 3) / 4, NZT = (2 * NZ + 7) / 8;
+  static constexpr int KF = (2 * P + 3) / 4, NFT = (2 * NG + 7) / 8;
+  static constexpr int KI = (2 * NG + 3) / 4, NIT = (2 * P + 7) / 8;
+};
+
+// fragment tables: [ks][nt][lane] twiddle block entries (host-built, see build_fft_m2l)
+template <int NKS, int NNT>
+__device__ __forceinline__ void load_wfrag(const double* __restrict__ tab, double (&w)[NKS][NNT]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < NKS; ++k)
+#pragma unroll
+    for (int n = 0; n < NNT; ++n) w[k][n] = tab[(k * NNT + n) * 32 + lane];
+}
+
+// one pass over nlines lines by the CTA's warps; loadA(line, k) -> double,
+// storeC(line, o, double2) for o < nout
+template <int NKS, int NNT, class LoadA, class StoreC>
+__device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __restrict__ wtab, LoadA loadA,
+                                         StoreC storeC) {
+  double w[NKS][NNT];
+  load_wfrag<NKS, NNT>(wtab, w);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  for (int mt = warp; mt * 8 < nlines; mt += nw) {
+    const int line = mt * 8 + g;
+    const bool ok = line < nlines;
+    double acc[NNT][2];
+#pragma unroll
+    for (int n = 0; n < NNT; ++n) acc[n][0] = acc[n][1] = 0.0;
+#pragma unroll
+    for (int k = 0; k < NKS; ++k) {
+      const double a = ok ? loadA(line, 4 * k + tq) : 0.0;
+#pragma unroll
+      for (int n = 0; n < NNT; ++n) dmma(acc[n][0], acc[n][1], a, w[k][n]);
+    }
+    if (ok) {
+#pragma unroll
+      for (int n = 0; n < NNT; ++n) {
+        const int o = 4 * n + tq;
+        if (o < nout) storeC(line, o, make_double2(acc[n][0], acc[n][1]));
+      }
+    }
+  }
+}
 
 // forward: one CTA per (source parent q, child octant c); the child's upward
 // equivalent density on the p^3 lattice (non-zero on the surface only) ->
-// its real DFT on the NG^3 grid, staged z (real -> half spectrum), y, x in
-// shared memory, written to ub[f][q][c kml + e].  A missing child writes zeros.
+// its real DFT on the NG^3 grid, z (real -> half spectrum), y, x passes on
+// the tensor cores, written to ub[f][q][c kml + e].  A missing child writes
+// zeros when the chunk's product reads parent blocks.
 template <int P>
 __global__ void __launch_bounds__(256)
     k_fft_fwd(const int32_t* __restrict__ qbox, const int32_t* __restrict__ child, int64_t nq,
               const double* __restrict__ ue, int ldn, int kml, const int16_t* __restrict__ lat, int M,
-              double2* __restrict__ ub, int zero_missing) {
+              double2* __restrict__ ub, int zero_missing, const double* __restrict__ wz,
+              const double* __restrict__ wf) {
   using D = FftDims<P>;
-  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF;
-  constexpr int GZ = (NZ + FT - 1) / FT, GG = (NG + FT - 1) / FT;
+  using S = DftShape<P>;
+  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ;
   extern __shared__ __align__(16) double sm[];
   double* cube = sm;
   double2* A = reinterpret_cast<double2*>(sm + D::CUBE);  // [x][y][fz]
   double2* B = A + P * P * NZ;                              // [x][fy][fz]
-  double2* tw = B + P * NG * NZ;                            // w^j = exp(-2 pi i j / NG)
+  const double* Ad = reinterpret_cast<const double*>(A);
+  const double* Bd = reinterpret_cast<const double*>(B);
   const int64_t q = blockIdx.x >> 3;
   const int c = blockIdx.x & 7, tid = threadIdx.x, bd = blockDim.x;
   const int R = 8 * kml;
@@ -134,115 +194,58 @@ __global__ void __launch_bounds__(256)
       for (int f = tid; f < NF; f += bd) ub[((int64_t)f * nq + q) * R + c * kml + e] = make_double2(0.0, 0.0);
     return;
   }
-  for (int j = tid; j < NG; j += bd) {
-    double sn, cs;
-    sincospi(2.0 * j / NG, &sn, &cs);
-    tw[j] = make_double2(cs, -sn);
-  }
   for (int e = 0; e < kml; ++e) {
     for (int i = tid; i < P * P * P; i += bd) cube[i] = 0.0;
     __syncthreads();
     for (int m = tid; m < M; m += bd)
       cube[(lat[3 * m] * P + lat[3 * m + 1]) * P + lat[3 * m + 2]] = ue[box * ldn + m * kml + e];
     __syncthreads();
-    for (int idx = tid; idx < GZ * P * P; idx += bd) {  // z: real -> half spectrum
-      const int g = idx / (P * P), xy = idx - g * P * P;
-      const double* cc = cube + xy * P;
-      double2 acc[FT];
-      int k[FT];
-#pragma unroll
-      for (int j = 0; j < FT; ++j) {
-        acc[j] = make_double2(0.0, 0.0);
-        k[j] = 0;
-      }
-#pragma unroll
-      for (int z = 0; z < P; ++z) {
-        const double v = cc[z];
-#pragma unroll
-        for (int j = 0; j < FT; ++j) {
-          const double2 w = tw[k[j]];
-          acc[j].x = fma(v, w.x, acc[j].x);
-          acc[j].y = fma(v, w.y, acc[j].y);
-          k[j] += g * FT + j;
-          if (k[j] >= NG) k[j] -= NG;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < FT; ++j)
-        if (g * FT + j < NZ) A[xy * NZ + g * FT + j] = acc[j];
-    }
+    dft_pass<S::KZ, S::NZT>(  // z: lines (x, y), real input
+        P * P, NZ, wz, [&](int line, int k) { return k < P ? cube[line * P + k] : 0.0; },
+        [&](int line, int o, double2 v) { A[line * NZ + o] = v; });
     __syncthreads();
-    for (int idx = tid; idx < GG * P * NZ; idx += bd) {  // y
-      const int g = idx / (P * NZ), r = idx - g * P * NZ, x = r / NZ, fz = r - x * NZ;
-      const double2* a = A + x * P * NZ + fz;
-      double2 acc[FT];
-      int k[FT];
-#pragma unroll
-      for (int j = 0; j < FT; ++j) {
-        acc[j] = make_double2(0.0, 0.0);
-        k[j] = 0;
-      }
-#pragma unroll
-      for (int y = 0; y < P; ++y) {
-        const double2 v = a[y * NZ];
-#pragma unroll
-        for (int j = 0; j < FT; ++j) {
-          cmac(acc[j], v, tw[k[j]]);
-          k[j] += g * FT + j;
-          if (k[j] >= NG) k[j] -= NG;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < FT; ++j)
-        if (g * FT + j < NG) B[(x * NG + g * FT + j) * NZ + fz] = acc[j];
-    }
+    dft_pass<S::KF, S::NFT>(  // y: lines (x, fz)
+        P * NZ, NG, wf,
+        [&](int line, int k) {
+          const int x = line / NZ, fz = line - x * NZ, y = k >> 1;
+          return y < P ? Ad[2 * ((x * P + y) * NZ + fz) + (k & 1)] : 0.0;
+        },
+        [&](int line, int o, double2 v) {
+          const int x = line / NZ, fz = line - x * NZ;
+          B[(x * NG + o) * NZ + fz] = v;
+        });
     __syncthreads();
-    for (int idx = tid; idx < GG * NG * NZ; idx += bd) {  // x
-      const int g = idx / (NG * NZ), r = idx - g * NG * NZ;
-      const double2* bb = B + r;
-      double2 acc[FT];
-      int k[FT];
-#pragma unroll
-      for (int j = 0; j < FT; ++j) {
-        acc[j] = make_double2(0.0, 0.0);
-        k[j] = 0;
-      }
-#pragma unroll
-      for (int x = 0; x < P; ++x) {
-        const double2 v = bb[x * NG * NZ];
-#pragma unroll
-        for (int j = 0; j < FT; ++j) {
-          cmac(acc[j], v, tw[k[j]]);
-          k[j] += g * FT + j;
-          if (k[j] >= NG) k[j] -= NG;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < FT; ++j) {
-        const int fx = g * FT + j;
-        if (fx < NG) ub[((int64_t)(fx * NG * NZ + r) * nq + q) * R + c * kml + e] = acc[j];
-      }
-    }
+    dft_pass<S::KF, S::NFT>(  // x: lines (fy, fz) -> global, frequency major
+        NGNZ, NG, wf,
+        [&](int line, int k) {
+          const int x = k >> 1;
+          return x < P ? Bd[2 * (x * NGNZ + line) + (k & 1)] : 0.0;
+        },
+        [&](int line, int o, double2 v) { ub[((int64_t)(o * NGNZ + line) * nq + q) * R + c * kml + e] = v; });
     __syncthreads();
   }
 }
 
 // inverse: one CTA per target box; its check spectrum cb[f][parent][b kml + a]
-// -> inverse DFT evaluated only at the downward-check surface points, times
-// 2^l / NG^3, added to CHK.  NG is odd, so there is no Nyquist bin.
+// -> x and y passes on the tensor cores (outputs only for x, y < p), the z
+// pass evaluated only at the downward-check surface points, times 2^l / NG^3,
+// added to CHK.  NG is odd, so there is no Nyquist bin.
 template <int P>
 __global__ void __launch_bounds__(256)
     k_fft_inv(const int32_t* __restrict__ tbox, const int2* __restrict__ tpb, int64_t npar,
               const int32_t* __restrict__ level, const double2* __restrict__ cb, int kml,
-              const int16_t* __restrict__ lat, int M, double* __restrict__ chk, int ldn) {
+              const int16_t* __restrict__ lat, int M, double* __restrict__ chk, int ldn,
+              const double* __restrict__ wi) {
   using D = FftDims<P>;
-  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF;
-  constexpr int GP = (P + FT - 1) / FT;
+  using S = DftShape<P>;
+  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ;
   extern __shared__ __align__(16) double sm[];
-  double2* S = reinterpret_cast<double2*>(sm);  // [fx][fy][fz], then E [x][y][fz]
-  double2* Dx = S + NF;                          // [x][fy][fz]
-  double2* tw = Dx + P * NG * NZ;                // exp(+2 pi i j / NG)
-  double2* E = S;
+  double2* Sp = reinterpret_cast<double2*>(sm);  // [fx][fy][fz], then E [x][y][fz]
+  double2* Dx = Sp + NF;                          // [x][fy][fz]
+  double2* tw = Dx + P * NG * NZ;                 // exp(+2 pi i j / NG)
+  double2* E = Sp;
+  const double* Sd = reinterpret_cast<const double*>(Sp);
+  const double* Dd = reinterpret_cast<const double*>(Dx);
   const int t = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
   const int64_t box = tbox[t];
   const int2 pb = tpb[t];
@@ -255,56 +258,26 @@ __global__ void __launch_bounds__(256)
   }
   for (int a = 0; a < kml; ++a) {
     const double2* col = cb + (int64_t)pb.x * R + pb.y * kml + a;
-    for (int f = tid; f < NF; f += bd) S[f] = col[(int64_t)f * npar * R];
+    for (int f = tid; f < NF; f += bd) Sp[f] = col[(int64_t)f * npar * R];
     __syncthreads();
-    for (int idx = tid; idx < GP * NG * NZ; idx += bd) {  // x: only x in [0, P)
-      const int g = idx / (NG * NZ), r = idx - g * NG * NZ;
-      double2 acc[FT];
-      int k[FT];
-#pragma unroll
-      for (int j = 0; j < FT; ++j) {
-        acc[j] = make_double2(0.0, 0.0);
-        k[j] = 0;
-      }
-#pragma unroll 4
-      for (int fx = 0; fx < NG; ++fx) {
-        const double2 v = S[fx * NG * NZ + r];
-#pragma unroll
-        for (int j = 0; j < FT; ++j) {
-          cmac(acc[j], v, tw[k[j]]);
-          k[j] += g * FT + j;
-          if (k[j] >= NG) k[j] -= NG;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < FT; ++j)
-        if (g * FT + j < P) Dx[(g * FT + j) * NG * NZ + r] = acc[j];
-    }
+    dft_pass<S::KI, S::NIT>(  // x: lines (fy, fz), outputs x < P
+        NGNZ, P, wi,
+        [&](int line, int k) {
+          const int fx = k >> 1;
+          return fx < NG ? Sd[2 * (fx * NGNZ + line) + (k & 1)] : 0.0;
+        },
+        [&](int line, int o, double2 v) { Dx[o * NGNZ + line] = v; });
     __syncthreads();
-    for (int idx = tid; idx < GP * P * NZ; idx += bd) {  // y: only y in [0, P)
-      const int g = idx / (P * NZ), r = idx - g * P * NZ, x = r / NZ, fz = r - x * NZ;
-      const double2* d = Dx + x * NG * NZ + fz;
-      double2 acc[FT];
-      int k[FT];
-#pragma unroll
-      for (int j = 0; j < FT; ++j) {
-        acc[j] = make_double2(0.0, 0.0);
-        k[j] = 0;
-      }
-#pragma unroll 4
-      for (int fy = 0; fy < NG; ++fy) {
-        const double2 v = d[fy * NZ];
-#pragma unroll
-        for (int j = 0; j < FT; ++j) {
-          cmac(acc[j], v, tw[k[j]]);
-          k[j] += g * FT + j;
-          if (k[j] >= NG) k[j] -= NG;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < FT; ++j)
-        if (g * FT + j < P) E[(x * P + g * FT + j) * NZ + fz] = acc[j];
-    }
+    dft_pass<S::KI, S::NIT>(  // y: lines (x, fz), outputs y < P
+        P * NZ, P, wi,
+        [&](int line, int k) {
+          const int x = line / NZ, fz = line - x * NZ, fy = k >> 1;
+          return fy < NG ? Dd[2 * ((x * NG + fy) * NZ + fz) + (k & 1)] : 0.0;
+        },
+        [&](int line, int o, double2 v) {
+          const int x = line / NZ, fz = line - x * NZ;
+          E[(x * P + o) * NZ + fz] = v;
+        });
     __syncthreads();
     double* o = chk + box * ldn;
     for (int m = tid; m < M; m += bd) {  // z: half spectrum -> real, only at surface points
@@ -321,12 +294,6 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
   }
-}
-
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
 }
 
 // Hadamard stage on the FP64 tensor cores.  For one frequency f and a target
@@ -508,7 +475,8 @@ template <int P>
 static void launch_fwd(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
   k_fft_fwd<P><<<(unsigned)(8 * ch.nq), 256, FftDims<P>::FWD_SMEM, Pl.stream>>>(
-      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lat, Pl.M, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1);
+      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lat, Pl.M, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1,
+      Pl.d_wz, Pl.d_wf);
   KF_CHECK_LAUNCH();
   Pl.launches++;
 }
@@ -516,7 +484,7 @@ template <int P>
 static void launch_inv(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
   k_fft_inv<P><<<(unsigned)ch.nt, 256, FftDims<P>::INV_SMEM, Pl.stream>>>(
-      ch.d_tbox, ch.d_tpb, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn);
+      ch.d_tbox, ch.d_tpb, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn, Pl.d_wi);
   KF_CHECK_LAUNCH();
   Pl.launches++;
 }
@@ -637,6 +605,40 @@ void build_fft_m2l(Plan& P, int64_t budget) {
     }
     P.d_aidx = dalloc<int16_t>(P, ai.size());
     KF_CUDA(cudaMemcpyAsync(P.d_aidx, ai.data(), ai.size() * 2, cudaMemcpyHostToDevice, st));
+  }
+  // DFT pass twiddle fragments (see dft_pass): [ks][nt][lane] of the real GEMM
+  // matrix B[(i, c_in)][(o, c_out)] = 2x2 real block of w^(s o i) (1x2 for real input)
+  {
+    const int NG = P.NG, NZ = P.NZ;
+    auto table = [&](int nin, int nout, bool cin, double sgn, std::vector<double>& t) {
+      const int kc = cin ? 2 : 1, K = kc * nin, N = 2 * nout;
+      const int NKS = (K + 3) / 4, NNT = (N + 7) / 8;
+      t.assign((size_t)NKS * NNT * 32, 0.0);
+      for (int ks = 0; ks < NKS; ++ks)
+        for (int nt = 0; nt < NNT; ++nt)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int k = 4 * ks + (lane & 3), n = 8 * nt + (lane >> 2);
+            const int i = k / kc, ci = k % kc, o = n / 2, co = n % 2;
+            double v = 0.0;
+            if (i < nin && o < nout) {
+              const double ang = sgn * 2.0 * M_PI * (double)(((int64_t)o * i) % NG) / NG;
+              const double wr = std::cos(ang), wi = std::sin(ang);
+              if (!cin) v = co == 0 ? wr : wi;
+              else v = (co == 0) ? (ci == 0 ? wr : -wi) : (ci == 0 ? wi : wr);
+            }
+            t[((size_t)ks * NNT + nt) * 32 + lane] = v;
+          }
+    };
+    std::vector<double> tz, tf, ti;
+    table(p, NZ, false, -1.0, tz);
+    table(p, NG, true, -1.0, tf);
+    table(NG, p, true, +1.0, ti);
+    P.d_wz = dalloc<double>(P, tz.size());
+    P.d_wf = dalloc<double>(P, tf.size());
+    P.d_wi = dalloc<double>(P, ti.size());
+    KF_CUDA(cudaMemcpyAsync(P.d_wz, tz.data(), tz.size() * 8, cudaMemcpyHostToDevice, st));
+    KF_CUDA(cudaMemcpyAsync(P.d_wf, tf.data(), tf.size() * 8, cudaMemcpyHostToDevice, st));
+    KF_CUDA(cudaMemcpyAsync(P.d_wi, ti.data(), ti.size() * 8, cudaMemcpyHostToDevice, st));
   }
   // integer lattice of the surface points (same order as d_surf)
   std::vector<int16_t> lat;

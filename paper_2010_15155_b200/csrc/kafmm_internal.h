@@ -170,6 +170,7 @@ struct Plan {
   double2* d_that = nullptr;       // [NF][316][ncomp] operator spectra at level 0
   int16_t* d_lat = nullptr;        // M x 3 integer lattice coordinates of the surface points
   int16_t* d_aidx = nullptr;       // DMMA A-fragment gather table [26][8kml/4][kml][32]
+  double *d_wz = nullptr, *d_wf = nullptr, *d_wi = nullptr;  // DFT-pass twiddle fragments
   std::vector<FftChunk> fft_chunks;
   double2* d_ub = nullptr;         // [NF][nq][8 kml] source spectra by parent block
   double2* d_cb = nullptr;         // [NF][npar][8 kml] target check spectra by parent block

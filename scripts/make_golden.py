@@ -21,8 +21,8 @@ from oracle import fmm as F  # noqa: E402
 from oracle.kernels import direct_sum  # noqa: E402
 from oracle.tree import Tree  # noqa: E402
 
-SAMPLE_LEAVES = {2: 12, 3: 12, 4: 10, 5: 6, 6: 2, 7: 2}
-DIRECT_TARGETS = {2: 400, 3: 300, 4: 200, 5: 96, 6: 200, 7: 200}
+SAMPLE_LEAVES = {2: 12, 3: 12, 4: 10, 5: 6, 6: 2, 7: 2, 8: 2, 9: 2}
+DIRECT_TARGETS = {2: 400, 3: 300, 4: 200, 5: 96, 6: 200, 7: 200, 8: 200, 9: 200}
 
 
 def main(cids):

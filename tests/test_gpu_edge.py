@@ -92,3 +92,21 @@ def test_superposition_and_scale_covariance_at_size():
     half = KAFMM(pts * 0.5, "stokeslet", 8, 50)
     h = half.eval(v1)
     assert float((h - 2 * a).norm() / h.norm()) < 1e-11
+
+
+@pytest.mark.parametrize("kernel", WL.KERNELS)
+def test_leaves_larger_than_one_thread_pass(kernel):
+    # leaves of up to 1100 points: the leaf kernels run several target passes per
+    # CTA (128 x TP targets each) over one shared source chunk; repeated evals agree
+    import torch
+    pts = np.concatenate([np.random.default_rng(8).random((1100, 3)) * 0.2 + 0.1,
+                          np.random.default_rng(9).random((400, 3))])
+    vals = WL.random_values(kernel, pts.shape[0], 10)
+    plan, out = run_gpu(pts, vals, kernel, 5, 1100)
+    src = torch.from_numpy(vals).cuda()
+    for _ in range(3):
+        again = plan.eval(src).cpu().numpy()
+        assert F.rel_l2(again, out) < 1e-12
+    ref = F.fmm(pts, vals, kernel, 5, 1100)["out"]
+    for lo, hi in F.blocks(kernel):
+        assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10

@@ -41,6 +41,8 @@ CASES = [
     ("C7_poly_regvel_omega", "stokes_reg_vel_omega", lambda: WL.make_points(WL.CONFIGS[7], 12000), 8, 150),
     # StokesRegVelOmega (Table VI) on an adaptive tree
     ("regvel_omega_clustered", "stokes_reg_vel_omega", lambda: _clustered(4000, 7), 6, 32),
+    # torque-free: omega = Omega^eps f has no self term, so the far field of the omega block is tested
+    ("regvel_omega_forces", "stokes_reg_vel_omega", lambda: _clustered(4000, 9), 6, 32),
     # LapPGradGrad (Table III), charges + dipoles on the paper's cloud (C8 shape)
     ("C8_pgradgrad", "laplace_pgradgrad", lambda: WL.make_points(WL.CONFIGS[8], 12000), 8, 150),
     ("pgradgrad_clustered", "laplace_pgradgrad", lambda: _clustered(5000, 8), 7, 30),
@@ -57,6 +59,8 @@ def case(request):
         vals = WL.make_values(WL.CONFIGS[POLY[name]], pts.shape[0])
     else:
         vals = WL.random_values(kernel, pts.shape[0], 17)
+    if name == "regvel_omega_forces":
+        vals[:, 3:6] = 0.0
     plan, gpu = run_gpu(pts, vals, kernel, p, cap)
     ref = F.fmm(pts, vals, kernel, p, cap, keep_internals=True)
     return dict(name=name, kernel=kernel, pts=pts, vals=vals, p=p, cap=cap, plan=plan, gpu=gpu, ref=ref)
