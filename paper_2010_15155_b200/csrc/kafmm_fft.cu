@@ -90,9 +90,13 @@ template <int P>
 struct FftDims {
   static constexpr int NG = 2 * P - 1, NZ = NG / 2 + 1, NF = NG * NG * NZ;
   static constexpr int CUBE = (P * P * P + 1) / 2 * 2;  // doubles, keep 16-B alignment after it
-  static constexpr size_t FWD_SMEM = (CUBE + 2 * (P * P * NZ + P * NG * NZ + NG)) * sizeof(double);
-  // spectrum column (later reused for the y-pass output) + x-pass output + twiddles
-  static constexpr size_t INV_SMEM = 2 * (NF + P * NG * NZ + NG) * sizeof(double);
+  // DFT-pass fragment table sizes (doubles): forward z, forward y/x, inverse x/y
+  static constexpr int TZ = 32 * ((P + 3) / 4) * ((2 * NZ + 7) / 8);
+  static constexpr int TF = 32 * ((2 * P + 3) / 4) * ((2 * NG + 7) / 8);
+  static constexpr int TI = 32 * ((2 * NG + 3) / 4) * ((2 * P + 7) / 8);
+  static constexpr size_t FWD_SMEM = (CUBE + 2 * (P * P * NZ + P * NG * NZ + NG) + TZ + TF) * sizeof(double);
+  // spectrum column (later reused for the y-pass output) + x-pass output + twiddles + table
+  static constexpr size_t INV_SMEM = (2 * (NF + P * NG * NZ + NG) + TI) * sizeof(double);
 };
 
 __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
@@ -123,23 +127,19 @@ struct DftShape {
   static constexpr int KI = (2 * NG + 3) / 4, NIT = (2 * P + 7) / 8;
 };
 
-// fragment tables: [ks][nt][lane] twiddle block entries (host-built, see build_fft_m2l)
-template <int NKS, int NNT>
-__device__ __forceinline__ void load_wfrag(const double* __restrict__ tab, double (&w)[NKS][NNT]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < NKS; ++k)
-#pragma unroll
-    for (int n = 0; n < NNT; ++n) w[k][n] = tab[(k * NNT + n) * 32 + lane];
+// fragment tables: [ks][nt][lane] twiddle block entries (host-built, see
+// build_fft_m2l), staged in shared memory by the CTA; a lane reads its own
+// entry right before each DMMA (conflict-free), which keeps the register
+// count low enough for more resident CTAs than holding the table in registers
+__device__ __forceinline__ void stage_table(double* __restrict__ dst, const double* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
 // one pass over nlines lines by the CTA's warps; loadA(line, k) -> double,
 // storeC(line, o, double2) for o < nout
 template <int NKS, int NNT, class LoadA, class StoreC>
-__device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __restrict__ wtab, LoadA loadA,
+__device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __restrict__ wsm, LoadA loadA,
                                          StoreC storeC) {
-  double w[NKS][NNT];
-  load_wfrag<NKS, NNT>(wtab, w);
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   for (int mt = warp; mt * 8 < nlines; mt += nw) {
@@ -152,7 +152,7 @@ __device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __r
     for (int k = 0; k < NKS; ++k) {
       const double a = ok ? loadA(line, 4 * k + tq) : 0.0;
 #pragma unroll
-      for (int n = 0; n < NNT; ++n) dmma(acc[n][0], acc[n][1], a, w[k][n]);
+      for (int n = 0; n < NNT; ++n) dmma(acc[n][0], acc[n][1], a, wsm[(k * NNT + n) * 32 + lane]);
     }
     if (ok) {
 #pragma unroll
@@ -194,6 +194,10 @@ __global__ void __launch_bounds__(256)
       for (int f = tid; f < NF; f += bd) ub[((int64_t)f * nq + q) * R + c * kml + e] = make_double2(0.0, 0.0);
     return;
   }
+  double* wzs = reinterpret_cast<double*>(B + P * NG * NZ + NG);
+  double* wfs = wzs + D::TZ;
+  stage_table(wzs, wz, D::TZ);
+  stage_table(wfs, wf, D::TF);
   for (int e = 0; e < kml; ++e) {
     for (int i = tid; i < P * P * P; i += bd) cube[i] = 0.0;
     __syncthreads();
@@ -201,11 +205,11 @@ __global__ void __launch_bounds__(256)
       cube[(lat[3 * m] * P + lat[3 * m + 1]) * P + lat[3 * m + 2]] = ue[box * ldn + m * kml + e];
     __syncthreads();
     dft_pass<S::KZ, S::NZT>(  // z: lines (x, y), real input
-        P * P, NZ, wz, [&](int line, int k) { return k < P ? cube[line * P + k] : 0.0; },
+        P * P, NZ, wzs, [&](int line, int k) { return k < P ? cube[line * P + k] : 0.0; },
         [&](int line, int o, double2 v) { A[line * NZ + o] = v; });
     __syncthreads();
     dft_pass<S::KF, S::NFT>(  // y: lines (x, fz)
-        P * NZ, NG, wf,
+        P * NZ, NG, wfs,
         [&](int line, int k) {
           const int x = line / NZ, fz = line - x * NZ, y = k >> 1;
           return y < P ? Ad[2 * ((x * P + y) * NZ + fz) + (k & 1)] : 0.0;
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(256)
         });
     __syncthreads();
     dft_pass<S::KF, S::NFT>(  // x: lines (fy, fz) -> global, frequency major
-        NGNZ, NG, wf,
+        NGNZ, NG, wfs,
         [&](int line, int k) {
           const int x = k >> 1;
           return x < P ? Bd[2 * (x * NGNZ + line) + (k & 1)] : 0.0;
@@ -244,6 +248,8 @@ __global__ void __launch_bounds__(256)
   double2* Dx = Sp + NF;                          // [x][fy][fz]
   double2* tw = Dx + P * NG * NZ;                 // exp(+2 pi i j / NG)
   double2* E = Sp;
+  double* wis = reinterpret_cast<double*>(tw + NG);
+  stage_table(wis, wi, D::TI);
   const double* Sd = reinterpret_cast<const double*>(Sp);
   const double* Dd = reinterpret_cast<const double*>(Dx);
   const int t = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(256)
     for (int f = tid; f < NF; f += bd) Sp[f] = col[(int64_t)f * npar * R];
     __syncthreads();
     dft_pass<S::KI, S::NIT>(  // x: lines (fy, fz), outputs x < P
-        NGNZ, P, wi,
+        NGNZ, P, wis,
         [&](int line, int k) {
           const int fx = k >> 1;
           return fx < NG ? Sd[2 * (fx * NGNZ + line) + (k & 1)] : 0.0;
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(256)
         [&](int line, int o, double2 v) { Dx[o * NGNZ + line] = v; });
     __syncthreads();
     dft_pass<S::KI, S::NIT>(  // y: lines (x, fz), outputs y < P
-        P * NZ, P, wi,
+        P * NZ, P, wis,
         [&](int line, int k) {
           const int x = line / NZ, fz = line - x * NZ, fy = k >> 1;
           return fy < NG ? Dd[2 * ((x * NG + fy) * NZ + fz) + (k & 1)] : 0.0;
