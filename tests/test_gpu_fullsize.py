@@ -28,7 +28,7 @@ def _run(cid):
     return spec, out, inf
 
 
-@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5, 6, 7, 8, 9])
 def test_fullsize_parity_at_sampled_targets(cid):
     path = os.path.join(GOLD, f"oracle_C{cid}.npz")
     if cid == 1:
