@@ -156,6 +156,10 @@ kafmm_status kafmm_get_list(kafmm_plan plan, int which, int32_t* tgt, int32_t* s
 
 /* Per-stage device times (ms) of the most recent kafmm_eval when stage
  * timing is on (kafmm_set_timing(plan, 1)); names via kafmm_stage_name.
+ * Mode 1 runs every stage on the plan's stream so that its events bracket
+ * only that stage (the near field then does not overlap the far field);
+ * mode 2 records only the total and the M2L product (slots 11, 12) and keeps
+ * the overlap; 0 turns timing off.
  * Slot 12 ("m2l_product") is the device time of the M2L product kernels
  * alone (the frequency-space DMMA products of the FFT variant, or the dense
  * DMMA GEMMs), a part of slot 4 ("m2l"). */

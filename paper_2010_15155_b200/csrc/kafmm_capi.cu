@@ -29,11 +29,15 @@ static int dims(int kernel, int* ks, int* kt) {
 static void free_plan(kafmm_plan_s* P) {
   if (!P) return;
   cudaStreamSynchronize(P->stream);
+  if (P->side) cudaStreamSynchronize(P->side);
   for (void* p : P->allocs) cudaFree(p);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : P->prod_ev)
     if (e) cudaEventDestroy(e);
+  if (P->side) cudaStreamDestroy(P->side);
+  if (P->ev_near_in) cudaEventDestroy(P->ev_near_in);
+  if (P->ev_near_out) cudaEventDestroy(P->ev_near_out);
   delete P;
 }
 }  // namespace kafmm
@@ -41,21 +45,21 @@ static void free_plan(kafmm_plan_s* P) {
 using namespace kafmm;
 
 static void collect_stage_times(Plan& P) {
-  Plan* plan = &P;
-  if (plan->timing) {
-    KF_CUDA(cudaEventSynchronize(plan->ev[ST_TOTAL]));
-    for (int s = 0; s < ST_TOTAL; ++s) KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[s], plan->ev[s], plan->ev[s + 1]));
-    KF_CUDA(cudaEventElapsedTime(&plan->stage_ms[ST_TOTAL], plan->ev[0], plan->ev[ST_TOTAL]));
-    float prod = 0.0f;
-    for (int i = 0; i + 1 < plan->prod_used; i += 2) {
-      float t = 0.0f;
-      KF_CUDA(cudaEventElapsedTime(&t, plan->prod_ev[i], plan->prod_ev[i + 1]));
-      prod += t;
-    }
-    plan->stage_ms[ST_M2L_PRODUCT] = prod;
+  if (!P.timing) return;
+  KF_CUDA(cudaEventSynchronize(P.ev[ST_TOTAL]));
+  if (P.timing == 1)
+    for (int s = 0; s < ST_TOTAL; ++s) KF_CUDA(cudaEventElapsedTime(&P.stage_ms[s], P.ev[s], P.ev[s + 1]));
+  else
+    for (int s = 0; s < ST_TOTAL; ++s) P.stage_ms[s] = 0.0f;
+  KF_CUDA(cudaEventElapsedTime(&P.stage_ms[ST_TOTAL], P.ev[0], P.ev[ST_TOTAL]));
+  float prod = 0.0f;
+  for (int i = 0; i + 1 < P.prod_used; i += 2) {
+    float t = 0.0f;
+    KF_CUDA(cudaEventElapsedTime(&t, P.prod_ev[i], P.prod_ev[i + 1]));
+    prod += t;
   }
+  P.stage_ms[ST_M2L_PRODUCT] = prod;
 }
-
 
 #define KF_API_BEGIN try {
 #define KF_API_END                                 \
@@ -135,6 +139,9 @@ kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int
   P->d_de = dalloc<double>(*P, (size_t)P->nbox * P->ldn);
   P->d_t = dalloc<double>(*P, (size_t)P->nbox * P->ldk);
   for (auto& e : P->ev) KF_CUDA(cudaEventCreate(&e));
+  KF_CUDA(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+  KF_CUDA(cudaEventCreateWithFlags(&P->ev_near_in, cudaEventDisableTiming));
+  KF_CUDA(cudaEventCreateWithFlags(&P->ev_near_out, cudaEventDisableTiming));
   KF_CUDA(cudaStreamSynchronize(P->stream));
   *out = P;
   return KAFMM_OK;
@@ -316,7 +323,8 @@ kafmm_status kafmm_get_list(kafmm_plan plan, int which, int32_t* tgt, int32_t* s
 
 kafmm_status kafmm_set_timing(kafmm_plan plan, int on) {
   if (!plan) return KAFMM_EINVAL;
-  plan->timing = on != 0;
+  if (on < 0 || on > 2) return KAFMM_EINVAL;
+  plan->timing = on;
   return KAFMM_OK;
 }
 

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(PT_THREADS)
                const int64_t* __restrict__ pbeg, const int64_t* __restrict__ pend, const double* __restrict__ pts,
                const int64_t* __restrict__ w_off, const int32_t* __restrict__ w_src, const double* __restrict__ ue,
                const double* __restrict__ de, int ldn, const double* __restrict__ surf, int M,
-               double* __restrict__ outs) {
+               double* __restrict__ outs, int add) {
   constexpr int CH = STREAM_DOUBLES / SSTR;
   __shared__ __align__(16) double ss[STREAM_DOUBLES];
   const int job = blockIdx.x, tid = threadIdx.x;
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(PT_THREADS)
     if (fill) run(fill);
 #pragma unroll
     for (int a = 0; a < K::KT; ++a) acc[0][a] += acc2[a];
-    tile_reduce_store<TP, K::KT>(z, acc, ss, outs + t0 * K::KT, false);
+    tile_reduce_store<TP, K::KT>(z, acc, ss, outs + t0 * K::KT, add != 0);
   }
 }
 
@@ -291,7 +291,7 @@ template <class K, int SREC, int TP>
 __global__ void __launch_bounds__(PT_THREADS)
     k_p2p(const int32_t* __restrict__ leaves, const int64_t* __restrict__ pbeg, const int64_t* __restrict__ pend,
           const double* __restrict__ rec, const int64_t* __restrict__ roff, const int2* __restrict__ rng,
-          double* __restrict__ outs) {
+          double* __restrict__ outs, int add) {
   constexpr int CH = STREAM_DOUBLES / SREC;
   __shared__ __align__(16) double ss[STREAM_DOUBLES];
   const int job = blockIdx.x;
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(PT_THREADS)
     if (fill) run(fill);
 #pragma unroll
     for (int a = 0; a < K::KT; ++a) acc[0][a] += acc2[a];
-    tile_reduce_store<TP, K::KT>(z, acc, ss, outs + t0 * K::KT, true);
+    tile_reduce_store<TP, K::KT>(z, acc, ss, outs + t0 * K::KT, add != 0);
   }
 }
 
@@ -384,12 +384,29 @@ static void launch_surface(Plan& P, const int32_t* jobs, int64_t njobs, const in
   P.launches++;
 }
 
+// a11 launch: P2P over the owned leaves on stream s, storing (first writer)
+// or adding to the sorted outputs
+template <class KST, int SREC>
+static void launch_p2p(Plan& P, cudaStream_t s, int add) {
+  const Jobs& J = P.J;
+  if (J.nleaf <= 0) return;
+  constexpr int TPS = TPof<KST>::v;
+  if (P.n >= 48 * P.nleaf)
+    k_p2p<KST, SREC, TPS><<<(unsigned)J.nleaf, PT_THREADS, 0, s>>>(J.leaf_ids, P.d_pbeg, P.d_pend, P.d_rec,
+                                                                   J.u_roff, J.u_rng, P.d_outs, add);
+  else
+    k_p2p<KST, SREC, 1><<<(unsigned)J.nleaf, PT_THREADS, 0, s>>>(J.leaf_ids, P.d_pbeg, P.d_pend, P.d_rec, J.u_roff,
+                                                                 J.u_rng, P.d_outs, add);
+  KF_CHECK_LAUNCH();
+  P.launches++;
+}
+
 // a1-a4: gather, S2M, UC2UE, M2M (upward pass)
-template <class KS, int SREC>
+template <class KS, class KST, int SREC>
 static void eval_up_impl(Plan& P, const double* d_src) {
   cudaStream_t st = P.stream;
   auto mark = [&](int s) {
-    if (P.timing) KF_CUDA(cudaEventRecord(P.ev[s], st));
+    if (P.timing == 1 || (P.timing == 2 && (s == ST_GATHER || s == ST_TOTAL))) KF_CUDA(cudaEventRecord(P.ev[s], st));
   };
   const Jobs& J = P.J;
   P.launches = 0;
@@ -397,6 +414,16 @@ static void eval_up_impl(Plan& P, const double* d_src) {
   k_gather<<<nblk(P.n), 256, 0, st>>>(d_src, P.d_pts, P.d_perm, P.n, P.ks, SREC, P.d_rec);
   KF_CHECK_LAUNCH();
   P.launches++;
+  // the near field needs only the gathered records: it runs on a side stream
+  // concurrently with the whole far-field chain (stage timing keeps one stream
+  // so that every stage's events bracket only its own kernels)
+  P.near_async = P.timing != 1 && P.side != nullptr && P.J.nleaf > 0;
+  if (P.near_async) {
+    KF_CUDA(cudaEventRecord(P.ev_near_in, st));
+    KF_CUDA(cudaStreamWaitEvent(P.side, P.ev_near_in, 0));
+    launch_p2p<KST, SREC>(P, P.side, 0);
+    KF_CUDA(cudaEventRecord(P.ev_near_out, P.side));
+  }
   KF_CUDA(cudaMemsetAsync(P.d_ue, 0, (size_t)P.nbox * P.ldn * 8, st));
   mark(ST_S2M);
   if (J.ns2m > 0) launch_surface<KS, SREC, false>(P, J.s2m_ids, J.ns2m, nullptr, nullptr, ALPHA_UC);
@@ -412,7 +439,7 @@ template <class KS, class KT_, class KST, int SREC>
 static void eval_down_impl(Plan& P, double* d_out) {
   cudaStream_t st = P.stream;
   auto mark = [&](int s) {
-    if (P.timing) KF_CUDA(cudaEventRecord(P.ev[s], st));
+    if (P.timing == 1 || (P.timing == 2 && (s == ST_GATHER || s == ST_TOTAL))) KF_CUDA(cudaEventRecord(P.ev[s], st));
   };
   const Jobs& J = P.J;
   KF_CUDA(cudaMemsetAsync(P.d_chk, 0, (size_t)P.nbox * P.ldn * 8, st));
@@ -439,12 +466,14 @@ static void eval_down_impl(Plan& P, double* d_out) {
   // TP targets per thread pays off for leaves of >= 48 points (C5-like); small
   // leaves keep one target per thread and more source slices
   const bool big = P.nleaf > 0 && P.n >= 48 * P.nleaf;
-  constexpr int TPT = TPof<KT_>::v, TPS = TPof<KST>::v, SST = (3 + KT_::KS + 1) / 2 * 2;
+  constexpr int TPT = TPof<KT_>::v, SST = (3 + KT_::KS + 1) / 2 * 2;
+  if (P.near_async) KF_CUDA(cudaStreamWaitEvent(st, P.ev_near_out, 0));  // P2P stored first
+  const int far_add = P.near_async ? 1 : 0;
   if (J.nleaf > 0) {
 #define KF_FAR(TP)                                                                                             \
   k_leaf_far<KT_, SST, TP><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(J.leaf_ids, P.d_level, P.d_ijk, P.d_pbeg,  \
                                                                     P.d_pend, P.d_pts, J.w_off, J.w_src, P.d_ue, \
-                                                                    P.d_de, P.ldn, P.d_surf, P.M, P.d_outs)
+                                                                    P.d_de, P.ldn, P.d_surf, P.M, P.d_outs, far_add)
     if (big) KF_FAR(TPT);
     else KF_FAR(1);
 #undef KF_FAR
@@ -452,16 +481,7 @@ static void eval_down_impl(Plan& P, double* d_out) {
     P.launches++;
   }
   mark(ST_P2P);
-  if (J.nleaf > 0) {
-    if (big)
-      k_p2p<KST, SREC, TPS><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(J.leaf_ids, P.d_pbeg, P.d_pend, P.d_rec,
-                                                                      J.u_roff, J.u_rng, P.d_outs);
-    else
-      k_p2p<KST, SREC, 1><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(J.leaf_ids, P.d_pbeg, P.d_pend, P.d_rec,
-                                                                    J.u_roff, J.u_rng, P.d_outs);
-    KF_CHECK_LAUNCH();
-    P.launches++;
-  }
+  if (!P.near_async) launch_p2p<KST, SREC>(P, st, 1);
   mark(ST_SCATTER);
   const double scale = (P.kml == 1) ? 1.0 / (4.0 * M_PI) : 1.0 / (8.0 * M_PI);
   const int64_t cnt = (J.phi - J.plo) * P.kt;
@@ -476,13 +496,13 @@ static void eval_down_impl(Plan& P, double* d_out) {
 
 void run_eval_up(Plan& P, const double* d_src) {
   switch (P.kernel) {
-    case KAFMM_LAPLACE_PGRAD: eval_up_impl<KL, 4>(P, d_src); break;
-    case KAFMM_STOKESLET: eval_up_impl<KG, 8>(P, d_src); break;
-    case KAFMM_RPY: eval_up_impl<KRPY, 8>(P, d_src); break;
-    case KAFMM_STOKES_REG_VEL: eval_up_impl<KGE, 8>(P, d_src); break;
-    case KAFMM_STOKES_REG_VEL_OMEGA: eval_up_impl<KGET, 12>(P, d_src); break;
-    case KAFMM_LAPLACE_PGRADGRAD: eval_up_impl<KLD, 8>(P, d_src); break;
-    case KAFMM_LAPLACE_QPGRADGRAD: eval_up_impl<KLQ, 12>(P, d_src); break;
+    case KAFMM_LAPLACE_PGRAD: eval_up_impl<KL, KLG, 4>(P, d_src); break;
+    case KAFMM_STOKESLET: eval_up_impl<KG, KG, 8>(P, d_src); break;
+    case KAFMM_RPY: eval_up_impl<KRPY, KRPYL, 8>(P, d_src); break;
+    case KAFMM_STOKES_REG_VEL: eval_up_impl<KGE, KGE, 8>(P, d_src); break;
+    case KAFMM_STOKES_REG_VEL_OMEGA: eval_up_impl<KGET, KGETW, 12>(P, d_src); break;
+    case KAFMM_LAPLACE_PGRADGRAD: eval_up_impl<KLD, KLDGG, 8>(P, d_src); break;
+    case KAFMM_LAPLACE_QPGRADGRAD: eval_up_impl<KLQ, KLQGG, 12>(P, d_src); break;
     default: throw Error{KAFMM_EINVAL, "unknown kernel"};
   }
 }

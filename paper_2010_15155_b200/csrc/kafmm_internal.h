@@ -107,7 +107,10 @@ struct Plan {
   int M = 0, neq = 0, ldn = 0;   // surface points, equivalent vector length, padded
   int kept_up = 0, kept_dn = 0, ldk = 0;
   cudaStream_t stream = 0;
-  bool timing = false;
+  cudaStream_t side = nullptr;         // near field (P2P) overlapped with the far-field chain
+  cudaEvent_t ev_near_in = nullptr, ev_near_out = nullptr;
+  bool near_async = false;             // P2P of the current eval runs on `side`
+  int timing = 0;                      // 0 off, 1 per-stage events (one stream), 2 total + M2L product only
   cudaEvent_t ev[ST_TOTAL + 1] = {};
   float stage_ms[ST_M2L_PRODUCT + 1] = {};
   std::vector<cudaEvent_t> prod_ev;  // start/stop pairs around the M2L product launches (timing on)

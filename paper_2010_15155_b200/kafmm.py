@@ -220,7 +220,8 @@ class KAFMM:
                "kafmm_get_list")
         return tgt[:n], src[:n]
 
-    def set_timing(self, on: bool):
+    def set_timing(self, on):
+        """False/0 off; True/1 per-stage events (serialised); 2 total + M2L product only (overlapped)."""
         _check(self.lib.kafmm_set_timing(self.h, int(on)), "kafmm_set_timing")
 
     def stage_times(self) -> dict:
