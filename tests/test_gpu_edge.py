@@ -110,3 +110,22 @@ def test_leaves_larger_than_one_thread_pass(kernel):
     ref = F.fmm(pts, vals, kernel, 5, 1100)["out"]
     for lo, hi in F.blocks(kernel):
         assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10
+
+
+@pytest.mark.parametrize("kernel", ["laplace_pgrad", "rpy"])
+def test_overlapped_and_serialised_evaluations_agree(kernel):
+    # timing mode 1 runs every stage on one stream; modes 0 and 2 overlap the near
+    # field with the far field on a side stream (P2P stores, L2T/M2T add)
+    import torch
+    pts = np.random.default_rng(13).random((20000, 3))
+    vals = WL.random_values(kernel, 20000, 14)
+    plan, out0 = run_gpu(pts, vals, kernel, 6, 40)
+    src = torch.from_numpy(vals).cuda()
+    for mode in (1, 2, 0):
+        plan.set_timing(mode)
+        out = plan.eval(src).cpu().numpy()
+        assert F.rel_l2(out, out0) < 1e-12
+        if mode:
+            st = plan.stage_times()
+            assert st["total"] > 0 and st["m2l_product"] > 0
+    plan.set_timing(0)
