@@ -164,69 +164,98 @@ __device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __r
   }
 }
 
-// forward: one CTA per (source parent q, child octant c); the child's upward
-// equivalent density on the p^3 lattice (non-zero on the surface only) ->
-// its real DFT on the NG^3 grid, z (real -> half spectrum), y, x passes on
-// the tensor cores, written to ub[f][q][c kml + e].  A missing child writes
-// zeros when the chunk's product reads parent blocks.
+// forward: one CTA per source parent block q.  Its transforms -- (existing
+// child c, component e) pairs -- run NB at a time (NB sized to ~170 KB of
+// shared memory): every child's upward equivalent density on the p^3 lattice
+// (non-zero on the surface only) -> its real DFT on the NG^3 grid, z (real ->
+// half spectrum), y, x passes on the tensor cores over the lines of all NB
+// transforms at once (transform index fastest, so the final stores of one
+// frequency are NB consecutive 16-B words of ub[f][q][c kml + e]).  Missing
+// children are zero-filled when the chunk's product reads parent blocks.
+constexpr int FWD_THREADS = 512;
+
 template <int P>
-__global__ void __launch_bounds__(256)
+struct FwdCfg {
+  using D = FftDims<P>;
+  static constexpr int PER = D::CUBE + 2 * (P * P * D::NZ + P * D::NG * D::NZ);  // doubles per transform
+  static constexpr int NB0 = (170 * 1024 / 8) / PER;
+  static constexpr int NB = NB0 < 1 ? 1 : (NB0 > 8 ? 8 : NB0);
+  static constexpr size_t SMEM = (size_t)(NB * PER + D::TZ + D::TF) * sizeof(double);
+};
+
+template <int P>
+__global__ void __launch_bounds__(FWD_THREADS)
     k_fft_fwd(const int32_t* __restrict__ qbox, const int32_t* __restrict__ child, int64_t nq,
               const double* __restrict__ ue, int ldn, int kml, const int16_t* __restrict__ lat, int M,
               double2* __restrict__ ub, int zero_missing, const double* __restrict__ wz,
               const double* __restrict__ wf) {
   using D = FftDims<P>;
   using S = DftShape<P>;
-  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ;
+  using C = FwdCfg<P>;
+  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ, NB = C::NB, PER = C::PER;
   extern __shared__ __align__(16) double sm[];
-  double* cube = sm;
-  double2* A = reinterpret_cast<double2*>(sm + D::CUBE);  // [x][y][fz]
-  double2* B = A + P * P * NZ;                              // [x][fy][fz]
-  const double* Ad = reinterpret_cast<const double*>(A);
-  const double* Bd = reinterpret_cast<const double*>(B);
-  const int64_t q = blockIdx.x >> 3;
-  const int c = blockIdx.x & 7, tid = threadIdx.x, bd = blockDim.x;
+  const int64_t q = blockIdx.x;
+  const int tid = threadIdx.x, bd = blockDim.x;
   const int R = 8 * kml;
-  const int64_t box = child[8 * (int64_t)qbox[q] + c];
-  if (box < 0) {  // the per-pair product never reads a missing child: zeros only for blocks
-    if (!zero_missing) return;
-    for (int e = 0; e < kml; ++e)
-      for (int f = tid; f < NF; f += bd) ub[((int64_t)f * nq + q) * R + c * kml + e] = make_double2(0.0, 0.0);
-    return;
+  int chs[8], nch = 0;
+  const int64_t qb = qbox[q];
+  for (int c = 0; c < 8; ++c) {
+    const int b = child[8 * qb + c];
+    if (b >= 0) chs[nch++] = c;
+    else if (zero_missing)  // the per-pair product never reads a missing child
+      for (int e = 0; e < kml; ++e)
+        for (int f = tid; f < NF; f += bd) ub[((int64_t)f * nq + q) * R + c * kml + e] = make_double2(0.0, 0.0);
   }
-  double* wzs = reinterpret_cast<double*>(B + P * NG * NZ + NG);
+  double* wzs = sm + NB * PER;
   double* wfs = wzs + D::TZ;
   stage_table(wzs, wz, D::TZ);
   stage_table(wfs, wf, D::TF);
-  for (int e = 0; e < kml; ++e) {
-    for (int i = tid; i < P * P * P; i += bd) cube[i] = 0.0;
+  const int ntr = nch * kml;
+  for (int g0 = 0; g0 < ntr; g0 += NB) {
+    const int nb = min(NB, ntr - g0);  // transforms in this group: g0 + t -> (child chs[../kml], e)
     __syncthreads();
-    for (int m = tid; m < M; m += bd)
-      cube[(lat[3 * m] * P + lat[3 * m + 1]) * P + lat[3 * m + 2]] = ue[box * ldn + m * kml + e];
+    for (int i = tid; i < nb * D::CUBE; i += bd) sm[(i / D::CUBE) * PER + i % D::CUBE] = 0.0;
     __syncthreads();
-    dft_pass<S::KZ, S::NZT>(  // z: lines (x, y), real input
-        P * P, NZ, wzs, [&](int line, int k) { return k < P ? cube[line * P + k] : 0.0; },
-        [&](int line, int o, double2 v) { A[line * NZ + o] = v; });
+    for (int i = tid; i < nb * M; i += bd) {
+      const int t = i / M, m = i - t * M, tr = g0 + t;
+      const int64_t box = child[8 * qb + chs[tr / kml]];
+      sm[t * PER + (lat[3 * m] * P + lat[3 * m + 1]) * P + lat[3 * m + 2]] = ue[box * ldn + m * kml + tr % kml];
+    }
     __syncthreads();
-    dft_pass<S::KF, S::NFT>(  // y: lines (x, fz)
-        P * NZ, NG, wfs,
-        [&](int line, int k) {
-          const int x = line / NZ, fz = line - x * NZ, y = k >> 1;
-          return y < P ? Ad[2 * ((x * P + y) * NZ + fz) + (k & 1)] : 0.0;
+    dft_pass<S::KZ, S::NZT>(  // z: lines (x, y; t), real input
+        P * P * nb, NZ, wzs,
+        [&](int L, int k) {
+          const int xy = L / nb, t = L - xy * nb;
+          return k < P ? sm[t * PER + xy * P + k] : 0.0;
         },
-        [&](int line, int o, double2 v) {
-          const int x = line / NZ, fz = line - x * NZ;
-          B[(x * NG + o) * NZ + fz] = v;
+        [&](int L, int o, double2 v) {
+          const int xy = L / nb, t = L - xy * nb;
+          reinterpret_cast<double2*>(sm + t * PER + D::CUBE)[xy * NZ + o] = v;
         });
     __syncthreads();
-    dft_pass<S::KF, S::NFT>(  // x: lines (fy, fz) -> global, frequency major
-        NGNZ, NG, wfs,
-        [&](int line, int k) {
-          const int x = k >> 1;
-          return x < P ? Bd[2 * (x * NGNZ + line) + (k & 1)] : 0.0;
+    dft_pass<S::KF, S::NFT>(  // y: lines (x, fz; t)
+        P * NZ * nb, NG, wfs,
+        [&](int L, int k) {
+          const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ, y = k >> 1;
+          const double* A = sm + t * PER + D::CUBE;
+          return y < P ? A[2 * ((x * P + y) * NZ + fz) + (k & 1)] : 0.0;
         },
-        [&](int line, int o, double2 v) { ub[((int64_t)(o * NGNZ + line) * nq + q) * R + c * kml + e] = v; });
+        [&](int L, int o, double2 v) {
+          const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ;
+          reinterpret_cast<double2*>(sm + t * PER + D::CUBE + 2 * P * P * NZ)[(x * NG + o) * NZ + fz] = v;
+        });
     __syncthreads();
+    dft_pass<S::KF, S::NFT>(  // x: lines (fy, fz; t) -> global, frequency major
+        NGNZ * nb, NG, wfs,
+        [&](int L, int k) {
+          const int r = L / nb, t = L - r * nb, x = k >> 1;
+          const double* B = sm + t * PER + D::CUBE + 2 * P * P * NZ;
+          return x < P ? B[2 * (x * NGNZ + r) + (k & 1)] : 0.0;
+        },
+        [&](int L, int o, double2 v) {
+          const int r = L / nb, t = L - r * nb, tr = g0 + t;
+          ub[((int64_t)(o * NGNZ + r) * nq + q) * R + chs[tr / kml] * kml + tr % kml] = v;
+        });
   }
 }
 
@@ -467,7 +496,7 @@ static void set_smem_attrs() {
   static bool done = false;
   if (done) return;
   KF_CUDA(cudaFuncSetAttribute(k_fft_fwd<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)FftDims<P>::FWD_SMEM));
+                               (int)FwdCfg<P>::SMEM));
   KF_CUDA(cudaFuncSetAttribute(k_fft_inv<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)FftDims<P>::INV_SMEM));
   done = true;
@@ -480,7 +509,7 @@ static bool chunk_uses_pairs(const Plan& Pl, const FftChunk& ch) {
 template <int P>
 static void launch_fwd(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
-  k_fft_fwd<P><<<(unsigned)(8 * ch.nq), 256, FftDims<P>::FWD_SMEM, Pl.stream>>>(
+  k_fft_fwd<P><<<(unsigned)ch.nq, FWD_THREADS, FwdCfg<P>::SMEM, Pl.stream>>>(
       ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lat, Pl.M, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1,
       Pl.d_wz, Pl.d_wf);
   KF_CHECK_LAUNCH();
