@@ -164,160 +164,188 @@ __device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __r
   }
 }
 
-// forward: one CTA per source parent block q.  Its transforms -- (existing
-// child c, component e) pairs -- run NB at a time (NB sized to ~170 KB of
-// shared memory): every child's upward equivalent density on the p^3 lattice
-// (non-zero on the surface only) -> its real DFT on the NG^3 grid, z (real ->
-// half spectrum), y, x passes on the tensor cores over the lines of all NB
-// transforms at once (transform index fastest, so the final stores of one
-// frequency are NB consecutive 16-B words of ub[f][q][c kml + e]).  Missing
-// children are zero-filled when the chunk's product reads parent blocks.
-constexpr int FWD_THREADS = 512;
-
+// forward: one CTA per (source parent block q, group of NB transform slots);
+// slot s = c kml + e is (child octant c, component e), the order of ub's last
+// index.  Each transform: the child's upward equivalent density on the p^3
+// lattice (non-zero on the surface only) -> its real DFT on the NG^3 grid,
+// z (real -> half spectrum), y, x passes on the tensor cores over the lines of
+// all NB transforms at once (transform index fastest, so one frequency's
+// stores are NB consecutive 16-B words).  A missing child's slots are
+// zero-filled when the chunk's product reads parent blocks, else skipped.
 template <int P>
 struct FwdCfg {
   using D = FftDims<P>;
   static constexpr int PER = D::CUBE + 2 * (P * P * D::NZ + P * D::NG * D::NZ);  // doubles per transform
-  static constexpr int NB0 = (170 * 1024 / 8) / PER;
-  static constexpr int NB = NB0 < 1 ? 1 : (NB0 > 8 ? 8 : NB0);
-  static constexpr size_t SMEM = (size_t)(NB * PER + D::TZ + D::TF) * sizeof(double);
+  template <int NB>
+  static constexpr size_t smem() { return (size_t)(NB * PER + D::TZ + D::TF) * sizeof(double); }
 };
 
-template <int P>
-__global__ void __launch_bounds__(FWD_THREADS)
+template <int P, int NB>
+__global__ void __launch_bounds__(256)
     k_fft_fwd(const int32_t* __restrict__ qbox, const int32_t* __restrict__ child, int64_t nq,
               const double* __restrict__ ue, int ldn, int kml, const int16_t* __restrict__ lat, int M,
               double2* __restrict__ ub, int zero_missing, const double* __restrict__ wz,
               const double* __restrict__ wf) {
   using D = FftDims<P>;
   using S = DftShape<P>;
-  using C = FwdCfg<P>;
-  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ, NB = C::NB, PER = C::PER;
+  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ, PER = FwdCfg<P>::PER;
   extern __shared__ __align__(16) double sm[];
-  const int64_t q = blockIdx.x;
-  const int tid = threadIdx.x, bd = blockDim.x;
   const int R = 8 * kml;
-  int chs[8], nch = 0;
+  const int ng = (R + NB - 1) / NB;
+  const int64_t q = blockIdx.x / ng;
+  const int s0 = (blockIdx.x % ng) * NB;
+  const int tid = threadIdx.x, bd = blockDim.x;
   const int64_t qb = qbox[q];
-  for (int c = 0; c < 8; ++c) {
-    const int b = child[8 * qb + c];
-    if (b >= 0) chs[nch++] = c;
-    else if (zero_missing)  // the per-pair product never reads a missing child
-      for (int e = 0; e < kml; ++e)
-        for (int f = tid; f < NF; f += bd) ub[((int64_t)f * nq + q) * R + c * kml + e] = make_double2(0.0, 0.0);
+  // this CTA's transforms: slots with an existing child (missing ones zero-filled / skipped)
+  int slot[NB];
+  int64_t bx[NB];
+  int nb = 0;
+  for (int j = 0; j < NB && s0 + j < R; ++j) {
+    const int sl = s0 + j;
+    const int64_t b = child[8 * qb + sl / kml];
+    if (b >= 0) {
+      slot[nb] = sl;
+      bx[nb] = b;
+      ++nb;
+    } else if (zero_missing) {
+      for (int f = tid; f < NF; f += bd) ub[((int64_t)f * nq + q) * R + sl] = make_double2(0.0, 0.0);
+    }
   }
+  if (nb == 0) return;
   double* wzs = sm + NB * PER;
   double* wfs = wzs + D::TZ;
   stage_table(wzs, wz, D::TZ);
   stage_table(wfs, wf, D::TF);
-  const int ntr = nch * kml;
-  for (int g0 = 0; g0 < ntr; g0 += NB) {
-    const int nb = min(NB, ntr - g0);  // transforms in this group: g0 + t -> (child chs[../kml], e)
-    __syncthreads();
-    for (int i = tid; i < nb * D::CUBE; i += bd) sm[(i / D::CUBE) * PER + i % D::CUBE] = 0.0;
-    __syncthreads();
-    for (int i = tid; i < nb * M; i += bd) {
-      const int t = i / M, m = i - t * M, tr = g0 + t;
-      const int64_t box = child[8 * qb + chs[tr / kml]];
-      sm[t * PER + (lat[3 * m] * P + lat[3 * m + 1]) * P + lat[3 * m + 2]] = ue[box * ldn + m * kml + tr % kml];
-    }
-    __syncthreads();
-    dft_pass<S::KZ, S::NZT>(  // z: lines (x, y; t), real input
-        P * P * nb, NZ, wzs,
-        [&](int L, int k) {
-          const int xy = L / nb, t = L - xy * nb;
-          return k < P ? sm[t * PER + xy * P + k] : 0.0;
-        },
-        [&](int L, int o, double2 v) {
-          const int xy = L / nb, t = L - xy * nb;
-          reinterpret_cast<double2*>(sm + t * PER + D::CUBE)[xy * NZ + o] = v;
-        });
-    __syncthreads();
-    dft_pass<S::KF, S::NFT>(  // y: lines (x, fz; t)
-        P * NZ * nb, NG, wfs,
-        [&](int L, int k) {
-          const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ, y = k >> 1;
-          const double* A = sm + t * PER + D::CUBE;
-          return y < P ? A[2 * ((x * P + y) * NZ + fz) + (k & 1)] : 0.0;
-        },
-        [&](int L, int o, double2 v) {
-          const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ;
-          reinterpret_cast<double2*>(sm + t * PER + D::CUBE + 2 * P * P * NZ)[(x * NG + o) * NZ + fz] = v;
-        });
-    __syncthreads();
-    dft_pass<S::KF, S::NFT>(  // x: lines (fy, fz; t) -> global, frequency major
-        NGNZ * nb, NG, wfs,
-        [&](int L, int k) {
-          const int r = L / nb, t = L - r * nb, x = k >> 1;
-          const double* B = sm + t * PER + D::CUBE + 2 * P * P * NZ;
-          return x < P ? B[2 * (x * NGNZ + r) + (k & 1)] : 0.0;
-        },
-        [&](int L, int o, double2 v) {
-          const int r = L / nb, t = L - r * nb, tr = g0 + t;
-          ub[((int64_t)(o * NGNZ + r) * nq + q) * R + chs[tr / kml] * kml + tr % kml] = v;
-        });
+  for (int i = tid; i < nb * D::CUBE; i += bd) sm[(i / D::CUBE) * PER + i % D::CUBE] = 0.0;
+  __syncthreads();
+  for (int i = tid; i < nb * M; i += bd) {
+    const int t = i / M, m = i - t * M;
+    int sl = slot[0];
+    int64_t b = bx[0];
+#pragma unroll
+    for (int j = 1; j < NB; ++j)
+      if (t == j) {
+        sl = slot[j];
+        b = bx[j];
+      }
+    sm[t * PER + (lat[3 * m] * P + lat[3 * m + 1]) * P + lat[3 * m + 2]] = ue[b * ldn + m * kml + sl % kml];
   }
+  __syncthreads();
+  dft_pass<S::KZ, S::NZT>(  // z: lines (x, y; t), real input
+      P * P * nb, NZ, wzs,
+      [&](int L, int k) {
+        const int xy = L / nb, t = L - xy * nb;
+        return k < P ? sm[t * PER + xy * P + k] : 0.0;
+      },
+      [&](int L, int o, double2 v) {
+        const int xy = L / nb, t = L - xy * nb;
+        reinterpret_cast<double2*>(sm + t * PER + D::CUBE)[xy * NZ + o] = v;
+      });
+  __syncthreads();
+  dft_pass<S::KF, S::NFT>(  // y: lines (x, fz; t)
+      P * NZ * nb, NG, wfs,
+      [&](int L, int k) {
+        const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ, y = k >> 1;
+        const double* A = sm + t * PER + D::CUBE;
+        return y < P ? A[2 * ((x * P + y) * NZ + fz) + (k & 1)] : 0.0;
+      },
+      [&](int L, int o, double2 v) {
+        const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ;
+        reinterpret_cast<double2*>(sm + t * PER + D::CUBE + 2 * P * P * NZ)[(x * NG + o) * NZ + fz] = v;
+      });
+  __syncthreads();
+  dft_pass<S::KF, S::NFT>(  // x: lines (fy, fz; t) -> global, frequency major
+      NGNZ * nb, NG, wfs,
+      [&](int L, int k) {
+        const int r = L / nb, t = L - r * nb, x = k >> 1;
+        const double* B = sm + t * PER + D::CUBE + 2 * P * P * NZ;
+        return x < P ? B[2 * (x * NGNZ + r) + (k & 1)] : 0.0;
+      },
+      [&](int L, int o, double2 v) {
+        const int r = L / nb, t = L - r * nb;
+        int sl = slot[0];
+#pragma unroll
+        for (int j = 1; j < NB; ++j)
+          if (t == j) sl = slot[j];
+        ub[((int64_t)(o * NGNZ + r) * nq + q) * R + sl] = v;
+      });
 }
 
-// inverse: one CTA per target box; its check spectrum cb[f][parent][b kml + a]
-// -> x and y passes on the tensor cores (outputs only for x, y < p), the z
-// pass evaluated only at the downward-check surface points, times 2^l / NG^3,
+// inverse: one CTA per target parent P; its transforms -- (target child b,
+// component a) -- run NB at a time: the check spectra cb[f][P][b kml + a] ->
+// x pass (read straight from global memory, lines r = (fy, fz), outputs
+// x < p) and y pass (outputs y < p) on the tensor cores, then the z pass
+// evaluated only at the downward-check surface points, times 2^l / NG^3,
 // added to CHK.  NG is odd, so there is no Nyquist bin.
+constexpr int INV_THREADS = 512;
+
 template <int P>
-__global__ void __launch_bounds__(256)
-    k_fft_inv(const int32_t* __restrict__ tbox, const int2* __restrict__ tpb, int64_t npar,
-              const int32_t* __restrict__ level, const double2* __restrict__ cb, int kml,
+struct InvCfg {
+  using D = FftDims<P>;
+  static constexpr int PER = 2 * (P * D::NG * D::NZ + P * P * D::NZ);  // doubles per transform: Dx, E
+  static constexpr int NB0 = (170 * 1024 / 8) / PER;
+  static constexpr int NB = NB0 < 1 ? 1 : (NB0 > 8 ? 8 : NB0);
+  static constexpr size_t SMEM = (size_t)(NB * PER + 2 * D::NG + D::TI) * sizeof(double);
+};
+
+template <int P>
+__global__ void __launch_bounds__(INV_THREADS)
+    k_fft_inv(const int32_t* __restrict__ tbox, const int2* __restrict__ tpb, const int32_t* __restrict__ toff,
+              int64_t npar, const int32_t* __restrict__ level, const double2* __restrict__ cb, int kml,
               const int16_t* __restrict__ lat, int M, double* __restrict__ chk, int ldn,
               const double* __restrict__ wi) {
   using D = FftDims<P>;
   using S = DftShape<P>;
-  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ;
+  using C = InvCfg<P>;
+  constexpr int NG = D::NG, NZ = D::NZ, NGNZ = NG * NZ, NB = C::NB, PER = C::PER;
   extern __shared__ __align__(16) double sm[];
-  double2* Sp = reinterpret_cast<double2*>(sm);  // [fx][fy][fz], then E [x][y][fz]
-  double2* Dx = Sp + NF;                          // [x][fy][fz]
-  double2* tw = Dx + P * NG * NZ;                 // exp(+2 pi i j / NG)
-  double2* E = Sp;
-  double* wis = reinterpret_cast<double*>(tw + NG);
-  stage_table(wis, wi, D::TI);
-  const double* Sd = reinterpret_cast<const double*>(Sp);
-  const double* Dd = reinterpret_cast<const double*>(Dx);
-  const int t = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
-  const int64_t box = tbox[t];
-  const int2 pb = tpb[t];
+  double2* tw = reinterpret_cast<double2*>(sm + NB * PER);  // exp(+2 pi i j / NG)
+  double* wis = sm + NB * PER + 2 * NG;
+  const int64_t par = blockIdx.x;
+  const int tid = threadIdx.x, bd = blockDim.x;
   const int R = 8 * kml;
-  const double scale = ldexp(1.0, level[box]) / (double)(NG * NG * NG);
+  const int t0 = toff[par], t1 = toff[par + 1];
+  if (t0 == t1) return;
+  const double scale = ldexp(1.0, level[tbox[t0]]) / (double)(NG * NG * NG);
   for (int j = tid; j < NG; j += bd) {
     double sn, cs;
     sincospi(2.0 * j / NG, &sn, &cs);
     tw[j] = make_double2(cs, sn);
   }
-  for (int a = 0; a < kml; ++a) {
-    const double2* col = cb + (int64_t)pb.x * R + pb.y * kml + a;
-    for (int f = tid; f < NF; f += bd) Sp[f] = col[(int64_t)f * npar * R];
+  stage_table(wis, wi, D::TI);
+  const double* cbd = reinterpret_cast<const double*>(cb);
+  const int ntr = (t1 - t0) * kml;
+  for (int g0 = 0; g0 < ntr; g0 += NB) {
+    const int nb = min(NB, ntr - g0);  // transform g0 + t -> target t0 + (g0 + t) / kml, component (g0 + t) % kml
     __syncthreads();
-    dft_pass<S::KI, S::NIT>(  // x: lines (fy, fz), outputs x < P
-        NGNZ, P, wis,
-        [&](int line, int k) {
-          const int fx = k >> 1;
-          return fx < NG ? Sd[2 * (fx * NGNZ + line) + (k & 1)] : 0.0;
+    dft_pass<S::KI, S::NIT>(  // x: lines (fy, fz; t), input straight from cb, outputs x < P
+        NGNZ * nb, P, wis,
+        [&](int L, int k) {
+          const int r = L / nb, t = L - r * nb, tr = g0 + t, fx = k >> 1;
+          const int slot = tpb[t0 + tr / kml].y * kml + tr % kml;
+          return fx < NG ? cbd[2 * (((int64_t)fx * NGNZ + r) * npar * R + par * R + slot) + (k & 1)] : 0.0;
         },
-        [&](int line, int o, double2 v) { Dx[o * NGNZ + line] = v; });
-    __syncthreads();
-    dft_pass<S::KI, S::NIT>(  // y: lines (x, fz), outputs y < P
-        P * NZ, P, wis,
-        [&](int line, int k) {
-          const int x = line / NZ, fz = line - x * NZ, fy = k >> 1;
-          return fy < NG ? Dd[2 * ((x * NG + fy) * NZ + fz) + (k & 1)] : 0.0;
-        },
-        [&](int line, int o, double2 v) {
-          const int x = line / NZ, fz = line - x * NZ;
-          E[(x * P + o) * NZ + fz] = v;
+        [&](int L, int o, double2 v) {
+          const int r = L / nb, t = L - r * nb;
+          reinterpret_cast<double2*>(sm + t * PER)[o * NGNZ + r] = v;
         });
     __syncthreads();
-    double* o = chk + box * ldn;
-    for (int m = tid; m < M; m += bd) {  // z: half spectrum -> real, only at surface points
-      int x = lat[3 * m], y = lat[3 * m + 1], z = lat[3 * m + 2];
-      const double2* e = E + (x * P + y) * NZ;
+    dft_pass<S::KI, S::NIT>(  // y: lines (x, fz; t), outputs y < P
+        P * NZ * nb, P, wis,
+        [&](int L, int k) {
+          const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ, fy = k >> 1;
+          const double* Dx = sm + t * PER;
+          return fy < NG ? Dx[2 * ((x * NG + fy) * NZ + fz) + (k & 1)] : 0.0;
+        },
+        [&](int L, int o, double2 v) {
+          const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ;
+          reinterpret_cast<double2*>(sm + t * PER + 2 * P * NG * NZ)[(x * P + o) * NZ + fz] = v;
+        });
+    __syncthreads();
+    for (int i = tid; i < nb * M; i += bd) {  // z: half spectrum -> real, only at surface points
+      const int t = i / M, m = i - t * M, tr = g0 + t;
+      const int x = lat[3 * m], y = lat[3 * m + 1], z = lat[3 * m + 2];
+      const double2* e = reinterpret_cast<const double2*>(sm + t * PER + 2 * P * NG * NZ) + (x * P + y) * NZ;
       double v = 0.0;
       int k = z;
       for (int fz = 1; fz < NZ; ++fz) {
@@ -325,9 +353,9 @@ __global__ void __launch_bounds__(256)
         k += z;
         if (k >= NG) k -= NG;
       }
-      o[m * kml + a] += scale * fma(2.0, v, e[0].x);
+      const int64_t box = tbox[t0 + tr / kml];
+      chk[box * ldn + m * kml + tr % kml] += scale * fma(2.0, v, e[0].x);
     }
-    __syncthreads();
   }
 }
 
@@ -491,35 +519,59 @@ __global__ void __launch_bounds__(PAIR_THREADS)
 // ---------------------------------------------------------------------------
 // host
 // ---------------------------------------------------------------------------
+static bool chunk_uses_pairs(const Plan& Pl, const FftChunk& ch) {
+  return Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < FFT_PAIR_FILL);
+}
+
+// transforms per forward CTA: 2 at p <= 10 (two CTAs of ~110 KB per SM), 1 above;
+// KAFMM_FWD_NB=1|2|4 overrides (tuning knob; profiles/)
+static int fwd_nb(int p) {
+  static const char* e = getenv("KAFMM_FWD_NB");
+  if (e) return atoi(e) >= 4 ? 4 : (atoi(e) >= 2 ? 2 : 1);
+  return p <= 10 ? 2 : 1;
+}
+
 template <int P>
 static void set_smem_attrs() {
   static bool done = false;
   if (done) return;
-  KF_CUDA(cudaFuncSetAttribute(k_fft_fwd<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)FwdCfg<P>::SMEM));
+  KF_CUDA(cudaFuncSetAttribute(k_fft_fwd<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)FwdCfg<P>::template smem<1>()));
+  if (FwdCfg<P>::template smem<2>() <= 227 * 1024)
+    KF_CUDA(cudaFuncSetAttribute(k_fft_fwd<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)FwdCfg<P>::template smem<2>()));
+  if (FwdCfg<P>::template smem<4>() <= 227 * 1024)
+    KF_CUDA(cudaFuncSetAttribute(k_fft_fwd<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)FwdCfg<P>::template smem<4>()));
   KF_CUDA(cudaFuncSetAttribute(k_fft_inv<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)FftDims<P>::INV_SMEM));
+                               (int)InvCfg<P>::SMEM));
   done = true;
 }
 
-static bool chunk_uses_pairs(const Plan& Pl, const FftChunk& ch) {
-  return Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < FFT_PAIR_FILL);
+template <int P, int NB>
+static void launch_fwd_nb(Plan& Pl, const FftChunk& ch) {
+  const int ng = (8 * Pl.kml + NB - 1) / NB;
+  k_fft_fwd<P, NB><<<(unsigned)(ch.nq * ng), 256, FwdCfg<P>::template smem<NB>(), Pl.stream>>>(
+      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lat, Pl.M, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1,
+      Pl.d_wz, Pl.d_wf);
 }
 
 template <int P>
 static void launch_fwd(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
-  k_fft_fwd<P><<<(unsigned)ch.nq, FWD_THREADS, FwdCfg<P>::SMEM, Pl.stream>>>(
-      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lat, Pl.M, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1,
-      Pl.d_wz, Pl.d_wf);
+  int nb = fwd_nb(P);
+  while (nb > 1 && (nb == 4 ? FwdCfg<P>::template smem<4>() : FwdCfg<P>::template smem<2>()) > 227 * 1024) nb /= 2;
+  if (nb == 4) launch_fwd_nb<P, 4>(Pl, ch);
+  else if (nb == 2) launch_fwd_nb<P, 2>(Pl, ch);
+  else launch_fwd_nb<P, 1>(Pl, ch);
   KF_CHECK_LAUNCH();
   Pl.launches++;
 }
 template <int P>
 static void launch_inv(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
-  k_fft_inv<P><<<(unsigned)ch.nt, 256, FftDims<P>::INV_SMEM, Pl.stream>>>(
-      ch.d_tbox, ch.d_tpb, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn, Pl.d_wi);
+  k_fft_inv<P><<<(unsigned)ch.npar, INV_THREADS, InvCfg<P>::SMEM, Pl.stream>>>(
+      ch.d_tbox, ch.d_tpb, ch.d_toff, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn, Pl.d_wi);
   KF_CHECK_LAUNCH();
   Pl.launches++;
 }
@@ -805,7 +857,8 @@ void build_fft_chunks(Plan& P, int64_t budget) {
       ch.nq = (int64_t)qs.size();
       std::vector<int32_t> tb;
       std::vector<int2> tpb;
-      for (int64_t q = 0; q < ch.npar; ++q)
+      std::vector<int32_t> toff(1, 0);
+      for (int64_t q = 0; q < ch.npar; ++q) {
         for (int o = 0; o < 8; ++o) {
           const int32_t c = child[8 * parents[i0 + q] + o];
           if (c >= 0 && (P.box_active.empty() || P.box_active[c])) {
@@ -813,6 +866,8 @@ void build_fft_chunks(Plan& P, int64_t budget) {
             tpb.push_back(make_int2((int)q, o));
           }
         }
+        toff.push_back((int32_t)tb.size());
+      }
       ch.nt = (int64_t)tb.size();
       std::vector<int64_t> ploff(1, 0);
       std::vector<int32_t> pl;
@@ -844,6 +899,8 @@ void build_fft_chunks(Plan& P, int64_t budget) {
       ch.d_nbr = dalloc<int32_t>(P, ch.npar * 26);
       ch.d_tbox = dalloc<int32_t>(P, std::max<int64_t>(1, ch.nt));
       ch.d_tpb = dalloc<int2>(P, std::max<int64_t>(1, ch.nt));
+      ch.d_toff = dalloc<int32_t>(P, toff.size());
+      KF_CUDA(cudaMemcpyAsync(ch.d_toff, toff.data(), toff.size() * 4, cudaMemcpyHostToDevice, st));
       if (ch.nq) KF_CUDA(cudaMemcpyAsync(ch.d_qbox, qs.data(), ch.nq * 4, cudaMemcpyHostToDevice, st));
       KF_CUDA(cudaMemcpyAsync(ch.d_nbr, nb.data(), ch.npar * 26 * 4, cudaMemcpyHostToDevice, st));
       if (ch.nt) {

@@ -58,6 +58,7 @@ struct FftChunk {
   int32_t* d_nbr = nullptr;   // npar x 26: local q of the colleague in direction d, or -1
   int32_t* d_tbox = nullptr;  // nt target box ids
   int2* d_tpb = nullptr;      // nt: (local parent index, child octant)
+  int32_t* d_toff = nullptr;  // npar + 1: targets of local parent P are [toff[P], toff[P+1])
   // the same V pairs as a per-target list (for sparse chunks): entry
   // (q * 8 + c) << 9 | offset id, source = child c of source parent q
   int64_t npairs = 0;
