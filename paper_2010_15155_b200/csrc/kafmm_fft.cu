@@ -271,81 +271,65 @@ __global__ void __launch_bounds__(256)
       });
 }
 
-// inverse: one CTA per target parent P; its transforms -- (target child b,
-// component a) -- run NB at a time: the check spectra cb[f][P][b kml + a] ->
-// x pass (read straight from global memory, lines r = (fy, fz), outputs
-// x < p) and y pass (outputs y < p) on the tensor cores, then the z pass
-// evaluated only at the downward-check surface points, times 2^l / NG^3,
+// inverse: one CTA per target box; its check spectrum cb[f][parent][b kml + a]
+// -> x and y passes on the tensor cores (outputs only for x, y < p), the z
+// pass evaluated only at the downward-check surface points, times 2^l / NG^3,
 // added to CHK.  NG is odd, so there is no Nyquist bin.
-constexpr int INV_THREADS = 512;
-
 template <int P>
-struct InvCfg {
-  using D = FftDims<P>;
-  static constexpr int PER = 2 * (P * D::NG * D::NZ + P * P * D::NZ);  // doubles per transform: Dx, E
-  static constexpr int NB0 = (170 * 1024 / 8) / PER;
-  static constexpr int NB = NB0 < 1 ? 1 : (NB0 > 8 ? 8 : NB0);
-  static constexpr size_t SMEM = (size_t)(NB * PER + 2 * D::NG + D::TI) * sizeof(double);
-};
-
-template <int P>
-__global__ void __launch_bounds__(INV_THREADS)
-    k_fft_inv(const int32_t* __restrict__ tbox, const int2* __restrict__ tpb, const int32_t* __restrict__ toff,
-              int64_t npar, const int32_t* __restrict__ level, const double2* __restrict__ cb, int kml,
+__global__ void __launch_bounds__(256)
+    k_fft_inv(const int32_t* __restrict__ tbox, const int2* __restrict__ tpb, int64_t npar,
+              const int32_t* __restrict__ level, const double2* __restrict__ cb, int kml,
               const int16_t* __restrict__ lat, int M, double* __restrict__ chk, int ldn,
               const double* __restrict__ wi) {
   using D = FftDims<P>;
   using S = DftShape<P>;
-  using C = InvCfg<P>;
-  constexpr int NG = D::NG, NZ = D::NZ, NGNZ = NG * NZ, NB = C::NB, PER = C::PER;
+  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ;
   extern __shared__ __align__(16) double sm[];
-  double2* tw = reinterpret_cast<double2*>(sm + NB * PER);  // exp(+2 pi i j / NG)
-  double* wis = sm + NB * PER + 2 * NG;
-  const int64_t par = blockIdx.x;
-  const int tid = threadIdx.x, bd = blockDim.x;
+  double2* Sp = reinterpret_cast<double2*>(sm);  // [fx][fy][fz], then E [x][y][fz]
+  double2* Dx = Sp + NF;                          // [x][fy][fz]
+  double2* tw = Dx + P * NG * NZ;                 // exp(+2 pi i j / NG)
+  double2* E = Sp;
+  double* wis = reinterpret_cast<double*>(tw + NG);
+  stage_table(wis, wi, D::TI);
+  const double* Sd = reinterpret_cast<const double*>(Sp);
+  const double* Dd = reinterpret_cast<const double*>(Dx);
+  const int t = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+  const int64_t box = tbox[t];
+  const int2 pb = tpb[t];
   const int R = 8 * kml;
-  const int t0 = toff[par], t1 = toff[par + 1];
-  if (t0 == t1) return;
-  const double scale = ldexp(1.0, level[tbox[t0]]) / (double)(NG * NG * NG);
+  const double scale = ldexp(1.0, level[box]) / (double)(NG * NG * NG);
   for (int j = tid; j < NG; j += bd) {
     double sn, cs;
     sincospi(2.0 * j / NG, &sn, &cs);
     tw[j] = make_double2(cs, sn);
   }
-  stage_table(wis, wi, D::TI);
-  const double* cbd = reinterpret_cast<const double*>(cb);
-  const int ntr = (t1 - t0) * kml;
-  for (int g0 = 0; g0 < ntr; g0 += NB) {
-    const int nb = min(NB, ntr - g0);  // transform g0 + t -> target t0 + (g0 + t) / kml, component (g0 + t) % kml
+  for (int a = 0; a < kml; ++a) {
+    const double2* col = cb + (int64_t)pb.x * R + pb.y * kml + a;
+    for (int f = tid; f < NF; f += bd) Sp[f] = col[(int64_t)f * npar * R];
     __syncthreads();
-    dft_pass<S::KI, S::NIT>(  // x: lines (fy, fz; t), input straight from cb, outputs x < P
-        NGNZ * nb, P, wis,
-        [&](int L, int k) {
-          const int r = L / nb, t = L - r * nb, tr = g0 + t, fx = k >> 1;
-          const int slot = tpb[t0 + tr / kml].y * kml + tr % kml;
-          return fx < NG ? cbd[2 * (((int64_t)fx * NGNZ + r) * npar * R + par * R + slot) + (k & 1)] : 0.0;
+    dft_pass<S::KI, S::NIT>(  // x: lines (fy, fz), outputs x < P
+        NGNZ, P, wis,
+        [&](int line, int k) {
+          const int fx = k >> 1;
+          return fx < NG ? Sd[2 * (fx * NGNZ + line) + (k & 1)] : 0.0;
         },
-        [&](int L, int o, double2 v) {
-          const int r = L / nb, t = L - r * nb;
-          reinterpret_cast<double2*>(sm + t * PER)[o * NGNZ + r] = v;
+        [&](int line, int o, double2 v) { Dx[o * NGNZ + line] = v; });
+    __syncthreads();
+    dft_pass<S::KI, S::NIT>(  // y: lines (x, fz), outputs y < P
+        P * NZ, P, wis,
+        [&](int line, int k) {
+          const int x = line / NZ, fz = line - x * NZ, fy = k >> 1;
+          return fy < NG ? Dd[2 * ((x * NG + fy) * NZ + fz) + (k & 1)] : 0.0;
+        },
+        [&](int line, int o, double2 v) {
+          const int x = line / NZ, fz = line - x * NZ;
+          E[(x * P + o) * NZ + fz] = v;
         });
     __syncthreads();
-    dft_pass<S::KI, S::NIT>(  // y: lines (x, fz; t), outputs y < P
-        P * NZ * nb, P, wis,
-        [&](int L, int k) {
-          const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ, fy = k >> 1;
-          const double* Dx = sm + t * PER;
-          return fy < NG ? Dx[2 * ((x * NG + fy) * NZ + fz) + (k & 1)] : 0.0;
-        },
-        [&](int L, int o, double2 v) {
-          const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ;
-          reinterpret_cast<double2*>(sm + t * PER + 2 * P * NG * NZ)[(x * P + o) * NZ + fz] = v;
-        });
-    __syncthreads();
-    for (int i = tid; i < nb * M; i += bd) {  // z: half spectrum -> real, only at surface points
-      const int t = i / M, m = i - t * M, tr = g0 + t;
-      const int x = lat[3 * m], y = lat[3 * m + 1], z = lat[3 * m + 2];
-      const double2* e = reinterpret_cast<const double2*>(sm + t * PER + 2 * P * NG * NZ) + (x * P + y) * NZ;
+    double* o = chk + box * ldn;
+    for (int m = tid; m < M; m += bd) {  // z: half spectrum -> real, only at surface points
+      int x = lat[3 * m], y = lat[3 * m + 1], z = lat[3 * m + 2];
+      const double2* e = E + (x * P + y) * NZ;
       double v = 0.0;
       int k = z;
       for (int fz = 1; fz < NZ; ++fz) {
@@ -353,9 +337,9 @@ __global__ void __launch_bounds__(INV_THREADS)
         k += z;
         if (k >= NG) k -= NG;
       }
-      const int64_t box = tbox[t0 + tr / kml];
-      chk[box * ldn + m * kml + tr % kml] += scale * fma(2.0, v, e[0].x);
+      o[m * kml + a] += scale * fma(2.0, v, e[0].x);
     }
+    __syncthreads();
   }
 }
 
@@ -523,12 +507,12 @@ static bool chunk_uses_pairs(const Plan& Pl, const FftChunk& ch) {
   return Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < FFT_PAIR_FILL);
 }
 
-// transforms per forward CTA: 2 at p <= 10 (two CTAs of ~110 KB per SM), 1 above;
+// transforms per forward CTA: 4 at p <= 10 (measured: C5 -3%, others equal), 1 above;
 // KAFMM_FWD_NB=1|2|4 overrides (tuning knob; profiles/)
 static int fwd_nb(int p) {
   static const char* e = getenv("KAFMM_FWD_NB");
   if (e) return atoi(e) >= 4 ? 4 : (atoi(e) >= 2 ? 2 : 1);
-  return p <= 10 ? 2 : 1;
+  return p <= 10 ? 4 : 1;
 }
 
 template <int P>
@@ -544,7 +528,7 @@ static void set_smem_attrs() {
     KF_CUDA(cudaFuncSetAttribute(k_fft_fwd<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)FwdCfg<P>::template smem<4>()));
   KF_CUDA(cudaFuncSetAttribute(k_fft_inv<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)InvCfg<P>::SMEM));
+                               (int)FftDims<P>::INV_SMEM));
   done = true;
 }
 
@@ -570,8 +554,8 @@ static void launch_fwd(Plan& Pl, const FftChunk& ch) {
 template <int P>
 static void launch_inv(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
-  k_fft_inv<P><<<(unsigned)ch.npar, INV_THREADS, InvCfg<P>::SMEM, Pl.stream>>>(
-      ch.d_tbox, ch.d_tpb, ch.d_toff, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn, Pl.d_wi);
+  k_fft_inv<P><<<(unsigned)ch.nt, 256, FftDims<P>::INV_SMEM, Pl.stream>>>(
+      ch.d_tbox, ch.d_tpb, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn, Pl.d_wi);
   KF_CHECK_LAUNCH();
   Pl.launches++;
 }
