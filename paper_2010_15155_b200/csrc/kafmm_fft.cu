@@ -588,10 +588,10 @@ void run_m2l_fft(Plan& Pl) {
       const unsigned grid = (unsigned)((int64_t)ntb * Pl.NF);
       if (Pl.kml == 1)
         k_m2l_pairs<1><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
-                                                             Pl.d_cb, ch.d_tpb, ch.d_pl_off, ch.d_pl);
+                                                             Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
       else
         k_m2l_pairs<3><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
-                                                             Pl.d_cb, ch.d_tpb, ch.d_pl_off, ch.d_pl);
+                                                             Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
     } else {
       // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
       // (fewer registers, more resident warps) -- a tuning knob measured in profiles/
@@ -853,9 +853,19 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         toff.push_back((int32_t)tb.size());
       }
       ch.nt = (int64_t)tb.size();
+      // per-pair product lists: targets ordered by child octant (the lanes of a warp then
+      // share one of the 8 V-offset patterns) and each list sorted by offset, so that
+      // lanes gather the same operator spectra at the same step where the tree is dense
+      std::vector<int32_t> tord(tb.size());
+      for (size_t i = 0; i < tb.size(); ++i) tord[i] = (int32_t)i;
+      std::stable_sort(tord.begin(), tord.end(), [&](int32_t a, int32_t b) { return tpb[a].y < tpb[b].y; });
+      std::vector<int2> tpb_pair(tb.size());
       std::vector<int64_t> ploff(1, 0);
       std::vector<int32_t> pl;
-      for (int32_t t : tb) {
+      for (size_t ii = 0; ii < tb.size(); ++ii) {
+        const int32_t t = tb[tord[ii]];
+        tpb_pair[ii] = tpb[tord[ii]];
+        const size_t first = pl.size();
         for (int64_t e = voff[t]; e < voff[t + 1]; ++e) {
           const int32_t sb = vsrc[e];
           const int32_t q = qlocal[parent[sb]];
@@ -866,6 +876,7 @@ void build_fft_chunks(Plan& P, int64_t budget) {
           if (q < 0 || oid < 0) throw Error{KAFMM_ECUDA, "FFT M2L: V source outside the chunk's parent blocks"};
           pl.push_back((int32_t)((q * 8 + c) << 9 | oid));
         }
+        std::sort(pl.begin() + first, pl.end(), [](int32_t a, int32_t b) { return (a & 511) < (b & 511); });
         ploff.push_back((int64_t)pl.size());
       }
       if ((int64_t)qs.size() * 8 >= (1 << 22)) throw Error{KAFMM_EINVAL, "FFT M2L chunk too large for pair indices"};
@@ -875,6 +886,9 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         for (int32_t v : nb) blocks += v >= 0;
         ch.block_fill = blocks ? (double)ch.npairs / (64.0 * (double)blocks) : 1.0;
       }
+      ch.d_tpb_pair = dalloc<int2>(P, std::max<size_t>(1, tpb_pair.size()));
+      if (!tpb_pair.empty())
+        KF_CUDA(cudaMemcpyAsync(ch.d_tpb_pair, tpb_pair.data(), tpb_pair.size() * 8, cudaMemcpyHostToDevice, st));
       ch.d_pl_off = dalloc<int64_t>(P, ploff.size());
       ch.d_pl = dalloc<int32_t>(P, std::max<size_t>(1, pl.size()));
       KF_CUDA(cudaMemcpyAsync(ch.d_pl_off, ploff.data(), ploff.size() * 8, cudaMemcpyHostToDevice, st));

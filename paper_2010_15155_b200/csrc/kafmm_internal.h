@@ -62,6 +62,7 @@ struct FftChunk {
   // the same V pairs as a per-target list (for sparse chunks): entry
   // (q * 8 + c) << 9 | offset id, source = child c of source parent q
   int64_t npairs = 0;
+  int2* d_tpb_pair = nullptr;   // nt: (parent, octant) of the pair lists' target order
   int64_t* d_pl_off = nullptr;  // nt + 1
   int32_t* d_pl = nullptr;      // npairs
   double block_fill = 1.0;      // V pairs / (8x8 child blocks the DMMA product runs)
