@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(256)
       });
 }
 
-// inverse: one CTA per target box; its check spectrum cb[f][parent][b kml + a]
+// inverse: one CTA per target box; its check spectrum cb[parent][b kml + a][f] (one contiguous row)
 // -> x and y passes on the tensor cores (outputs only for x, y < p), the z
 // pass evaluated only at the downward-check surface points, times 2^l / NG^3,
 // added to CHK.  NG is odd, so there is no Nyquist bin.
@@ -304,8 +304,8 @@ __global__ void __launch_bounds__(256)
     tw[j] = make_double2(cs, sn);
   }
   for (int a = 0; a < kml; ++a) {
-    const double2* col = cb + (int64_t)pb.x * R + pb.y * kml + a;
-    for (int f = tid; f < NF; f += bd) Sp[f] = col[(int64_t)f * npar * R];
+    const double2* col = cb + ((int64_t)pb.x * R + pb.y * kml + a) * NF;  // target-major: one contiguous row
+    for (int f = tid; f < NF; f += bd) Sp[f] = col[f];
     __syncthreads();
     dft_pass<S::KI, S::NIT>(  // x: lines (fy, fz), outputs x < P
         NGNZ, P, wis,
@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
     k_m2l_dmma(int64_t npar, int64_t nq, int npb, const double2* __restrict__ that, const double2* __restrict__ ub,
                double2* __restrict__ cb, const int32_t* __restrict__ nbr, const int16_t* __restrict__ aidx) {
   constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML, KS = R / 4, PPW = NT * 8;
+  const int64_t NF = gridDim.x / npb;  // grid = parent blocks x frequency bins
   __shared__ double2 sT[N_OFFSETS * NC];
   const int64_t f = blockIdx.x / npb;
   const int pb = blockIdx.x % npb;
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       }
     }
   }
-  double2* cbf = cb + f * npar * R;
+  double2* cbf = cb + f;  // cb is target-major [parent][8 kml][NF]
 #pragma unroll
   for (int m = 0; m < KML; ++m)
 #pragma unroll
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t Pn = P0 + n * 8 + 2 * tq + e;
-        if (Pn < npar) cbf[Pn * R + m * 8 + g] = make_double2(acc[m][n][0][e], acc[m][n][1][e]);
+        if (Pn < npar) cbf[(Pn * R + m * 8 + g) * NF] = make_double2(acc[m][n][0][e], acc[m][n][1][e]);
       }
 }
 
@@ -444,6 +445,7 @@ __global__ void __launch_bounds__(PAIR_THREADS)
                 const double2* __restrict__ ub, double2* __restrict__ cb, const int2* __restrict__ tpb,
                 const int64_t* __restrict__ off, const int32_t* __restrict__ pl) {
   constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
+  const int64_t NF = gridDim.x / ntb;  // grid = target blocks x frequency bins
   // operator spectra of this frequency as NC planes of 316 complex: lanes that
   // gather different offsets spread over 8 bank groups (a 96-B record stride
   // would hit only 4)
@@ -495,9 +497,9 @@ __global__ void __launch_bounds__(PAIR_THREADS)
     }
   }
   const int2 pb = tpb[t];
-  double2* o = cb + (f * npar + pb.x) * R + pb.y * KML;
+  double2* o = cb + ((int64_t)pb.x * R + pb.y * KML) * NF + f;
 #pragma unroll
-  for (int a = 0; a < KML; ++a) o[a] = acc[a];
+  for (int a = 0; a < KML; ++a) o[(int64_t)a * NF] = acc[a];
 }
 
 // ---------------------------------------------------------------------------
@@ -853,19 +855,14 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         toff.push_back((int32_t)tb.size());
       }
       ch.nt = (int64_t)tb.size();
-      // per-pair product lists: targets ordered by child octant (the lanes of a warp then
-      // share one of the 8 V-offset patterns) and each list sorted by offset, so that
-      // lanes gather the same operator spectra at the same step where the tree is dense
-      std::vector<int32_t> tord(tb.size());
-      for (size_t i = 0; i < tb.size(); ++i) tord[i] = (int32_t)i;
-      std::stable_sort(tord.begin(), tord.end(), [&](int32_t a, int32_t b) { return tpb[a].y < tpb[b].y; });
-      std::vector<int2> tpb_pair(tb.size());
+      // per-pair product lists in the chunk's target order (Morton; measured better than
+      // grouping targets by octant and sorting lists by offset, which lost the locality
+      // of the source spectra reads: C5 product 1340 -> 1858 ms)
+      std::vector<int2> tpb_pair(tpb);
       std::vector<int64_t> ploff(1, 0);
       std::vector<int32_t> pl;
       for (size_t ii = 0; ii < tb.size(); ++ii) {
-        const int32_t t = tb[tord[ii]];
-        tpb_pair[ii] = tpb[tord[ii]];
-        const size_t first = pl.size();
+        const int32_t t = tb[ii];
         for (int64_t e = voff[t]; e < voff[t + 1]; ++e) {
           const int32_t sb = vsrc[e];
           const int32_t q = qlocal[parent[sb]];
@@ -876,7 +873,6 @@ void build_fft_chunks(Plan& P, int64_t budget) {
           if (q < 0 || oid < 0) throw Error{KAFMM_ECUDA, "FFT M2L: V source outside the chunk's parent blocks"};
           pl.push_back((int32_t)((q * 8 + c) << 9 | oid));
         }
-        std::sort(pl.begin() + first, pl.end(), [](int32_t a, int32_t b) { return (a & 511) < (b & 511); });
         ploff.push_back((int64_t)pl.size());
       }
       if ((int64_t)qs.size() * 8 >= (1 << 22)) throw Error{KAFMM_EINVAL, "FFT M2L chunk too large for pair indices"};

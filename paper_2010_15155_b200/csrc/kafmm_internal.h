@@ -178,7 +178,7 @@ struct Plan {
   double *d_wz = nullptr, *d_wf = nullptr, *d_wi = nullptr;  // DFT-pass twiddle fragments
   std::vector<FftChunk> fft_chunks;
   double2* d_ub = nullptr;         // [NF][nq][8 kml] source spectra by parent block
-  double2* d_cb = nullptr;         // [NF][npar][8 kml] target check spectra by parent block
+  double2* d_cb = nullptr;         // [npar][8 kml][NF] target check spectra, target-major (contiguous per target)
   int64_t fft_max_nq = 0, fft_max_npar = 0, fft_budget = 0;
 
   Jobs J;
