@@ -277,6 +277,27 @@ def main():
             stages.append(plan.stage_times())
         barrier()
     clocks = clk.summary()
+    # CUDA-graph replay of the same evaluation (launch overhead removed), timed
+    # the same way but without per-kernel events: reported beside `value`
+    graph_ms = None
+    if world == 1 and not args.dist:
+        plan.set_timing(0)
+        plan.set_graph(True)
+        run_step()
+        run_step()
+        gt = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run_step()
+            e1.record(stream)
+            e1.synchronize()
+            gt.append(e0.elapsed_time(e1))
+        plan.set_graph(False)
+        graph_ms = statistics.mean(gt)
     # one more evaluation with per-stage events (mode 1 serialises the near
     # field) for the breakdown and the P2P kernel time; not part of `value`
     plan.set_timing(1)
@@ -372,6 +393,7 @@ def main():
         "stages_note": ("per-stage events of one extra evaluation with the stages serialised (the timed steps run "
                         "the near field concurrently with the far field)"),
         "fft_m2l": plan.fft_stats() if mode.startswith("fft") else None,
+        "cuda_graph": None if graph_ms is None else {"ms_per_step": graph_ms, "value": 2 * spec.n / (graph_ms * 1e-3)},
         "clocks": clocks,
         "gpu_launches": launches,
         "e2e": e2e,

@@ -186,6 +186,13 @@ kafmm_status kafmm_get_m2l_mode(kafmm_plan plan, int* mode);
  * spectra budget in bytes. */
 kafmm_status kafmm_fft_stats(kafmm_plan plan, int64_t* st);
 
+/* CUDA graph replay of kafmm_eval (on = 1): the first evaluation with a given
+ * (src_values, trg_out, M2L mode) is captured into a graph on an internal
+ * stream, later ones with the same pointers replay it; the plan's stream is
+ * joined by events, so ordering is unchanged for the caller.  Ignored while
+ * stage timing is on.  Default off. */
+kafmm_status kafmm_set_graph(kafmm_plan plan, int on);
+
 /* Kernel launches issued by one kafmm_eval. */
 kafmm_status kafmm_launch_count(kafmm_plan plan, int* n);
 

@@ -30,12 +30,17 @@ static void free_plan(kafmm_plan_s* P) {
   if (!P) return;
   cudaStreamSynchronize(P->stream);
   if (P->side) cudaStreamSynchronize(P->side);
+  if (P->gstream) cudaStreamSynchronize(P->gstream);
+  if (P->gexec) cudaGraphExecDestroy(P->gexec);
   for (void* p : P->allocs) cudaFree(p);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : P->prod_ev)
     if (e) cudaEventDestroy(e);
   if (P->side) cudaStreamDestroy(P->side);
+  if (P->gstream) cudaStreamDestroy(P->gstream);
+  if (P->ev_gin) cudaEventDestroy(P->ev_gin);
+  if (P->ev_gout) cudaEventDestroy(P->ev_gout);
   if (P->ev_near_in) cudaEventDestroy(P->ev_near_in);
   if (P->ev_near_out) cudaEventDestroy(P->ev_near_out);
   delete P;
@@ -140,6 +145,9 @@ kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int
   P->d_t = dalloc<double>(*P, (size_t)P->nbox * P->ldk);
   for (auto& e : P->ev) KF_CUDA(cudaEventCreate(&e));
   KF_CUDA(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+  KF_CUDA(cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking));
+  KF_CUDA(cudaEventCreateWithFlags(&P->ev_gin, cudaEventDisableTiming));
+  KF_CUDA(cudaEventCreateWithFlags(&P->ev_gout, cudaEventDisableTiming));
   KF_CUDA(cudaEventCreateWithFlags(&P->ev_near_in, cudaEventDisableTiming));
   KF_CUDA(cudaEventCreateWithFlags(&P->ev_near_out, cudaEventDisableTiming));
   KF_CUDA(cudaStreamSynchronize(P->stream));
@@ -171,10 +179,49 @@ kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_o
     return KAFMM_EINVAL;
   }
   KF_API_BEGIN
-  run_eval(*plan, src_values, trg_out);
-  collect_stage_times(*plan);
+  Plan& P = *plan;
+  if (P.use_graph && P.timing == 0 && P.graph_warm) {
+    if (!P.gexec || P.g_src != src_values || P.g_out != trg_out || P.g_mode != P.m2l_mode) {
+      if (P.gexec) KF_CUDA(cudaGraphExecDestroy(P.gexec));
+      P.gexec = nullptr;
+      cudaStream_t user = P.stream;
+      P.stream = P.gstream;
+      cudaGraph_t g = nullptr;
+      KF_CUDA(cudaStreamBeginCapture(P.gstream, cudaStreamCaptureModeThreadLocal));
+      try {
+        run_eval(P, src_values, trg_out);
+      } catch (...) {
+        cudaStreamEndCapture(P.gstream, &g);
+        if (g) cudaGraphDestroy(g);
+        P.stream = user;
+        throw;
+      }
+      KF_CUDA(cudaStreamEndCapture(P.gstream, &g));
+      P.stream = user;
+      KF_CUDA(cudaGraphInstantiate(&P.gexec, g, 0));
+      KF_CUDA(cudaGraphDestroy(g));
+      P.g_src = src_values;
+      P.g_out = trg_out;
+      P.g_mode = P.m2l_mode;
+    }
+    KF_CUDA(cudaEventRecord(P.ev_gin, P.stream));
+    KF_CUDA(cudaStreamWaitEvent(P.gstream, P.ev_gin, 0));
+    KF_CUDA(cudaGraphLaunch(P.gexec, P.gstream));
+    KF_CUDA(cudaEventRecord(P.ev_gout, P.gstream));
+    KF_CUDA(cudaStreamWaitEvent(P.stream, P.ev_gout, 0));
+    return KAFMM_OK;
+  }
+  run_eval(P, src_values, trg_out);  // (also the first, uncaptured, evaluation of graph mode:
+  P.graph_warm = true;                // one-time kernel attribute setup happens outside capture)
+  collect_stage_times(P);
   return KAFMM_OK;
   KF_API_END
+}
+
+kafmm_status kafmm_set_graph(kafmm_plan plan, int on) {
+  if (!plan) return KAFMM_EINVAL;
+  plan->use_graph = on != 0;
+  return KAFMM_OK;
 }
 
 kafmm_status kafmm_eval_host(kafmm_plan plan, const double* src_values, double* trg_out) {

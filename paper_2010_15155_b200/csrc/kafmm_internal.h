@@ -112,6 +112,15 @@ struct Plan {
   cudaStream_t side = nullptr;         // near field (P2P) overlapped with the far-field chain
   cudaEvent_t ev_near_in = nullptr, ev_near_out = nullptr;
   bool near_async = false;             // P2P of the current eval runs on `side`
+  // CUDA graph of one evaluation (kafmm_set_graph): captured on `cap` for a
+  // given (src, out, M2L mode) and replayed; the caller's stream is joined by events
+  bool use_graph = false, graph_warm = false;
+  cudaStream_t gstream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const double* g_src = nullptr;
+  double* g_out = nullptr;
+  int g_mode = -1;
+  cudaEvent_t ev_gin = nullptr, ev_gout = nullptr;
   int timing = 0;                      // 0 off, 1 per-stage events (one stream), 2 total + M2L product only
   cudaEvent_t ev[ST_TOTAL + 1] = {};
   float stage_ms[ST_M2L_PRODUCT + 1] = {};

@@ -65,6 +65,7 @@ _SIGS = [
     ("kafmm_set_m2l_mode", C.c_int, [C.c_void_p, C.c_int]),
     ("kafmm_get_m2l_mode", C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     ("kafmm_fft_stats", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kafmm_set_graph", C.c_int, [C.c_void_p, C.c_int]),
     ("kafmm_restrict", C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
     ("kafmm_eval_up", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kafmm_eval_down", C.c_int, [C.c_void_p, C.c_void_p]),
@@ -268,6 +269,10 @@ class KAFMM:
         _check(self.lib.kafmm_scatter_rows(self.h, C.c_void_p(src.data_ptr()), int(dst.shape[1]),
                                            C.c_void_p(idx.data_ptr()), int(idx.numel()), C.c_void_p(dst.data_ptr())),
                "kafmm_scatter_rows")
+
+    def set_graph(self, on: bool):
+        """Replay evaluations from a captured CUDA graph (same src/out pointers)."""
+        _check(self.lib.kafmm_set_graph(self.h, int(bool(on))), "kafmm_set_graph")
 
     def fft_stats(self) -> dict:
         st = np.zeros(8, np.int64)

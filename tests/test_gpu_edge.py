@@ -129,3 +129,26 @@ def test_overlapped_and_serialised_evaluations_agree(kernel):
             st = plan.stage_times()
             assert st["total"] > 0 and st["m2l_product"] > 0
     plan.set_timing(0)
+
+
+def test_cuda_graph_replay_matches_and_follows_inputs():
+    import torch
+    from paper_2010_15155_b200 import KAFMM
+    pts = np.random.default_rng(15).random((6000, 3))
+    v1 = WL.random_values("stokeslet", 6000, 16)
+    v2 = WL.random_values("stokeslet", 6000, 17)
+    plan = KAFMM(pts, "stokeslet", 6, 40)
+    a = torch.from_numpy(v1).cuda()
+    ref1 = plan.eval(a).cpu().numpy()
+    plan.set_graph(True)
+    out = torch.empty_like(a)
+    for _ in range(3):                      # warm (uncaptured), capture, replay
+        plan.eval(a, out)
+        assert F.rel_l2(out.cpu().numpy(), ref1) < 1e-12
+    a.copy_(torch.from_numpy(v2))           # same pointers, new values: the replay reads them
+    plan.eval(a, out)
+    ref2 = F.fmm(pts, v2, "stokeslet", 6, 40)["out"]
+    assert F.rel_l2(out.cpu().numpy(), ref2) <= 1e-10
+    b = torch.from_numpy(v1).cuda()         # new pointer: re-captured
+    assert F.rel_l2(plan.eval(b).cpu().numpy(), ref1) < 1e-12
+    plan.set_graph(False)
