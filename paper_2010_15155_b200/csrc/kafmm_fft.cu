@@ -376,57 +376,50 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[m][n][0][0] = acc[m][n][0][1] = acc[m][n][1][0] = acc[m][n][1][1] = 0.0;
   const double2* ubf = ub + f * nq * R;
-  // B fragments of direction d+1 are loaded while direction d's DMMAs run
-  // (software pipelining over the 26 directions)
-  auto load_dir = [&](int d, double2 (&u)[KS][NT], bool& any) {
-    any = false;
+  int qn[NT];  // colleague block of the next direction (prefetched)
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const int64_t Pn = P0 + n * 8 + g;
+    qn[n] = Pn < npar ? nbr[Pn * 26] : -1;
+  }
+  for (int d = 0; d < 26; ++d) {
+    int64_t qb[NT];
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
+      qb[n] = qn[n] >= 0 ? (int64_t)qn[n] * R + tq : -1;
       const int64_t Pn = P0 + n * 8 + g;
-      const int qq = Pn < npar ? nbr[Pn * 26 + d] : -1;
-      any |= qq >= 0;
-      const double2* src = ubf + (int64_t)(qq >= 0 ? qq : 0) * R + tq;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) u[ks][n] = qq >= 0 ? src[ks * 4] : make_double2(0.0, 0.0);
+      qn[n] = (d + 1 < 26 && Pn < npar) ? nbr[Pn * 26 + d + 1] : -1;
     }
-  };
-  double2 ucur[KS][NT], unext[KS][NT];
-  bool anycur, anynext = false;
-  load_dir(0, ucur, anycur);
-  for (int d = 0; d < 26; ++d) {
-    if (d + 1 < 26) load_dir(d + 1, unext, anynext);
-    // a direction none of the warp's parents has a (non-leaf) colleague in: no work
-    if (__any_sync(0xffffffffu, anycur)) {
-      const int16_t* ai_tab = aidx + d * KS * KML * 32 + lane;
+    {  // a direction none of the warp's parents has a (non-leaf) colleague in: no work
+      bool any = false;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        double ar[KML], ai[KML], an[KML];
+      for (int n = 0; n < NT; ++n) any |= qb[n] >= 0;
+      if (!__any_sync(0xffffffffu, any)) continue;
+    }
+    const int16_t* ai_tab = aidx + d * KS * KML * 32 + lane;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      double ar[KML], ai[KML], an[KML];
+#pragma unroll
+      for (int m = 0; m < KML; ++m) {
+        const int idx = ai_tab[(ks * KML + m) * 32];
+        const double2 t = idx >= 0 ? sT[idx] : make_double2(0.0, 0.0);
+        ar[m] = t.x;
+        ai[m] = t.y;
+        an[m] = -t.y;
+      }
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const double2 u = qb[n] >= 0 ? ubf[qb[n] + ks * 4] : make_double2(0.0, 0.0);
 #pragma unroll
         for (int m = 0; m < KML; ++m) {
-          const int idx = ai_tab[(ks * KML + m) * 32];
-          const double2 t = idx >= 0 ? sT[idx] : make_double2(0.0, 0.0);
-          ar[m] = t.x;
-          ai[m] = t.y;
-          an[m] = -t.y;
-        }
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          const double2 u = ucur[ks][n];
-#pragma unroll
-          for (int m = 0; m < KML; ++m) {
-            dmma(acc[m][n][0][0], acc[m][n][0][1], ar[m], u.x);
-            dmma(acc[m][n][0][0], acc[m][n][0][1], an[m], u.y);
-            dmma(acc[m][n][1][0], acc[m][n][1][1], ar[m], u.y);
-            dmma(acc[m][n][1][0], acc[m][n][1][1], ai[m], u.x);
-          }
+          dmma(acc[m][n][0][0], acc[m][n][0][1], ar[m], u.x);
+          dmma(acc[m][n][0][0], acc[m][n][0][1], an[m], u.y);
+          dmma(acc[m][n][1][0], acc[m][n][1][1], ar[m], u.y);
+          dmma(acc[m][n][1][0], acc[m][n][1][1], ai[m], u.x);
         }
       }
     }
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-      for (int n = 0; n < NT; ++n) ucur[ks][n] = unext[ks][n];
-    anycur = anynext;
   }
   double2* cbf = cb + f;  // cb is target-major [parent][8 kml][NF]
 #pragma unroll
