@@ -502,6 +502,88 @@ __global__ void __launch_bounds__(PAIR_THREADS)
   for (int a = 0; a < KML; ++a) o[(int64_t)a * NF] = acc[a];
 }
 
+// The per-pair product for sparse Stokes-family chunks on the FP64 tensor
+// cores.  A tile of up to OG_TT targets is handled per (tile, frequency): its
+// V pairs are grouped by offset o (a target has at most one source per
+// offset, so a group's 8 columns are 8 distinct targets), and a group of <= 8
+// pairs is one real GEMM C[6 x 8] = A_o[6 x 6] B[6 x 8] padded to two
+// DMMA.8x8x4 (rows/cols: component x re|im; A = the 2x2 real blocks of the
+// operator spectrum T_o(f), B = the sources' spectra).  The tile's source
+// spectra and the frequency's operator spectra are staged in shared memory;
+// each warp accumulates into its own copy of the tile's outputs (no atomics:
+// within a warp the columns of a group are distinct targets), summed at the end.
+constexpr int OG_TT = 64, OG_NSMAX = 1024, OG_WARPS = 8;
+constexpr size_t OG_SMEM = (size_t)(6 * N_OFFSETS + OG_NSMAX * 3 + OG_WARPS * OG_TT * 3) * sizeof(double2);
+
+__global__ void __launch_bounds__(OG_WARPS * 32)
+    k_m2l_ogroups(int64_t nq, int64_t npar, int ntile, const double2* __restrict__ that,
+                  const double2* __restrict__ ub, double2* __restrict__ cb, const int2* __restrict__ tpb,
+                  const int32_t* __restrict__ tile_t0, const int32_t* __restrict__ tile_soff,
+                  const int32_t* __restrict__ tile_src, const int32_t* __restrict__ tile_goff,
+                  const int16_t* __restrict__ grp_o, const int32_t* __restrict__ grp_pairs) {
+  constexpr int R = 24;
+  extern __shared__ __align__(16) double2 og[];
+  double2* sT = og;                          // [6][316] planar
+  double2* sU = sT + 6 * N_OFFSETS;          // [ns][3]
+  double2* sacc = sU + OG_NSMAX * 3;         // [warp][OG_TT][3]
+  const int64_t NF = gridDim.x / ntile;
+  const int64_t f = blockIdx.x / ntile;
+  const int tile = blockIdx.x % ntile;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int t0 = tile_t0[tile], nt = tile_t0[tile + 1] - t0;
+  const int s0 = tile_soff[tile], ns = tile_soff[tile + 1] - s0;
+  const int g0 = tile_goff[tile], g1 = tile_goff[tile + 1];
+  for (int i = tid; i < N_OFFSETS * 6; i += bd) sT[(i % 6) * N_OFFSETS + i / 6] = that[f * N_OFFSETS * 6 + i];
+  const double2* ubf = ub + f * nq * R;
+  for (int i = tid; i < ns * 3; i += bd) sU[i] = ubf[(int64_t)tile_src[s0 + i / 3] * 3 + i % 3];
+  for (int i = tid; i < OG_WARPS * OG_TT * 3; i += bd) sacc[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+  const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+  double2* myacc = sacc + warp * OG_TT * 3;
+  // this lane's fixed A/B fragment coordinates: row g = (a, re|im), k = 4 ks + tq = (e, re|im)
+  const int ra = g >> 1, rr = g & 1;
+  for (int gi = g0 + warp; gi < g1; gi += OG_WARPS) {
+    const int o = grp_o[gi];
+    const int pw = grp_pairs[gi * 8 + g];  // column g of the B fragment: (t_local << 16) | source
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int k = 4 * ks + tq, e = k >> 1, kc = k & 1;
+      double a = 0.0, b = 0.0;
+      if (ra < 3 && e < 3) {
+        const double2 T = sT[sym[ra][e] * N_OFFSETS + o];
+        a = rr == 0 ? (kc == 0 ? T.x : -T.y) : (kc == 0 ? T.y : T.x);
+      }
+      if (pw >= 0 && e < 3) {
+        const double2 U = sU[(pw & 0xffff) * 3 + e];
+        b = kc == 0 ? U.x : U.y;
+      }
+      dmma(c0, c1, a, b);
+    }
+    if (ra < 3) {
+      const int p0 = grp_pairs[gi * 8 + 2 * tq], p1 = grp_pairs[gi * 8 + 2 * tq + 1];
+      // lanes g = 2a and 2a + 1 update the re and im words of one entry: 8-B accesses only
+      double* accd = reinterpret_cast<double*>(myacc);
+      if (p0 >= 0) accd[2 * ((p0 >> 16) * 3 + ra) + rr] += c0;
+      if (p1 >= 0) accd[2 * ((p1 >> 16) * 3 + ra) + rr] += c1;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nt * 3; i += bd) {
+    double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int w = 0; w < OG_WARPS; ++w) {
+      const double2 x = sacc[w * OG_TT * 3 + i];
+      v.x += x.x;
+      v.y += x.y;
+    }
+    const int t = t0 + i / 3, a = i % 3;
+    const int2 pb = tpb[t];
+    cb[((int64_t)pb.x * R + pb.y * 3 + a) * NF + f] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host
 // ---------------------------------------------------------------------------
@@ -588,12 +670,23 @@ void run_m2l_fft(Plan& Pl) {
     if (pairs) {
       const int ntb = (int)((ch.nt + PAIR_THREADS - 1) / PAIR_THREADS);
       const unsigned grid = (unsigned)((int64_t)ntb * Pl.NF);
+      static const bool scalar_pairs = getenv("KAFMM_SCALAR_PAIRS") != nullptr;  // A/B knob (profiles/)
       if (Pl.kml == 1)
         k_m2l_pairs<1><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
                                                              Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
-      else
+      else if (scalar_pairs || ch.ntile == 0)
         k_m2l_pairs<3><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
                                                              Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
+      else {
+        static bool attr = false;
+        if (!attr) {
+          KF_CUDA(cudaFuncSetAttribute(k_m2l_ogroups, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OG_SMEM));
+          attr = true;
+        }
+        k_m2l_ogroups<<<(unsigned)((int64_t)ch.ntile * Pl.NF), OG_WARPS * 32, OG_SMEM, Pl.stream>>>(
+            ch.nq, ch.npar, ch.ntile, Pl.d_that, Pl.d_ub, Pl.d_cb, ch.d_tpb, ch.d_og_t0, ch.d_og_soff, ch.d_og_src,
+            ch.d_og_goff, ch.d_og_o, ch.d_og_pairs);
+      }
     } else {
       // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
       // (fewer registers, more resident warps) -- a tuning knob measured in profiles/
@@ -619,6 +712,13 @@ void run_m2l_fft(Plan& Pl) {
     Pl.launches++;
     KF_FFT_DISPATCH(launch_inv);
   }
+}
+
+template <class T>
+static T* h2d_vec(Plan& P, const std::vector<T>& h) {
+  T* d = dalloc<T>(P, std::max<size_t>(1, h.size()));
+  if (!h.empty()) KF_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, P.stream));
+  return d;
 }
 
 template <class T>
@@ -881,6 +981,60 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         int64_t blocks = 0;
         for (int32_t v : nb) blocks += v >= 0;
         ch.block_fill = blocks ? (double)ch.npairs / (64.0 * (double)blocks) : 1.0;
+      }
+      if (P.kml == 3) {
+        // offset-grouped tiles for k_m2l_ogroups: up to OG_TT consecutive targets whose
+        // distinct sources fit OG_NSMAX; pairs sorted by offset, runs cut into groups of 8
+        std::vector<int32_t> t0v(1, 0), soff(1, 0), srcs, goff(1, 0), gp;
+        std::vector<int16_t> go;
+        std::vector<int32_t> mark(std::max<int64_t>(1, (int64_t)qs.size() * 8), -1);
+        std::vector<int64_t> rec;  // (oid << 32) | (t_local << 16) | local source
+        size_t t = 0;
+        while (t < tb.size()) {
+          const size_t ts = t;
+          std::vector<int32_t> tsrc;
+          while (t < tb.size() && (int)(t - ts) < OG_TT) {
+            int add = 0;
+            for (int64_t e = ploff[t]; e < ploff[t + 1]; ++e) add += mark[pl[e] >> 9] < 0;
+            if (t > ts && (int)tsrc.size() + add > OG_NSMAX) break;
+            for (int64_t e = ploff[t]; e < ploff[t + 1]; ++e) {
+              const int32_t qc = pl[e] >> 9;
+              if (mark[qc] < 0) {
+                mark[qc] = (int32_t)tsrc.size();
+                tsrc.push_back(qc);
+              }
+            }
+            ++t;
+          }
+          if ((int)tsrc.size() > OG_NSMAX) throw Error{KAFMM_ECUDA, "FFT M2L: a target with more V sources than a tile holds"};
+          rec.clear();
+          for (size_t u = ts; u < t; ++u)
+            for (int64_t e = ploff[u]; e < ploff[u + 1]; ++e)
+              rec.push_back(((int64_t)(pl[e] & 511) << 32) | ((int64_t)(u - ts) << 16) | mark[pl[e] >> 9]);
+          std::sort(rec.begin(), rec.end());
+          size_t i = 0;
+          while (i < rec.size()) {
+            const int o = (int)(rec[i] >> 32);
+            go.push_back((int16_t)o);
+            int k = 0;
+            for (; k < 8 && i < rec.size() && (int)(rec[i] >> 32) == o; ++k, ++i) gp.push_back((int32_t)(rec[i] & 0xffffffff));
+            for (; k < 8; ++k) gp.push_back(-1);
+          }
+          for (int32_t qc : tsrc) {
+            srcs.push_back(qc);
+            mark[qc] = -1;
+          }
+          t0v.push_back((int32_t)t);
+          soff.push_back((int32_t)srcs.size());
+          goff.push_back((int32_t)go.size());
+        }
+        ch.ntile = (int)(t0v.size() - 1);
+        ch.d_og_t0 = h2d_vec(P, t0v);
+        ch.d_og_soff = h2d_vec(P, soff);
+        ch.d_og_src = h2d_vec(P, srcs);
+        ch.d_og_goff = h2d_vec(P, goff);
+        ch.d_og_o = h2d_vec(P, go);
+        ch.d_og_pairs = h2d_vec(P, gp);
       }
       ch.d_tpb_pair = dalloc<int2>(P, std::max<size_t>(1, tpb_pair.size()));
       if (!tpb_pair.empty())
