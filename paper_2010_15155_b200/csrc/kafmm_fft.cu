@@ -512,8 +512,9 @@ __global__ void __launch_bounds__(PAIR_THREADS)
 // spectra and the frequency's operator spectra are staged in shared memory;
 // each warp accumulates into its own copy of the tile's outputs (no atomics:
 // within a warp the columns of a group are distinct targets), summed at the end.
-constexpr int OG_TT = 64, OG_NSMAX = 1024, OG_WARPS = 8;
-constexpr size_t OG_SMEM = (size_t)(6 * N_OFFSETS + OG_NSMAX * 3 + OG_WARPS * OG_TT * 3) * sizeof(double2);
+constexpr int OG_TT = 64, OG_NSMAX = 512, OG_WARPS = 4, OG_GCH = 256;
+constexpr size_t OG_SMEM = (size_t)(6 * N_OFFSETS + OG_NSMAX * 3 + OG_WARPS * OG_TT * 3) * sizeof(double2) +
+                           (size_t)OG_GCH * (8 * sizeof(int32_t) + sizeof(int32_t));
 
 __global__ void __launch_bounds__(OG_WARPS * 32)
     k_m2l_ogroups(int64_t nq, int64_t npar, int ntile, const double2* __restrict__ that,
@@ -523,9 +524,11 @@ __global__ void __launch_bounds__(OG_WARPS * 32)
                   const int16_t* __restrict__ grp_o, const int32_t* __restrict__ grp_pairs) {
   constexpr int R = 24;
   extern __shared__ __align__(16) double2 og[];
-  double2* sT = og;                          // [6][316] planar
-  double2* sU = sT + 6 * N_OFFSETS;          // [ns][3]
-  double2* sacc = sU + OG_NSMAX * 3;         // [warp][OG_TT][3]
+  double2* sT = og;                                    // [6][316] planar
+  double2* sU = sT + 6 * N_OFFSETS;                    // [ns][3]
+  double2* sacc = sU + OG_NSMAX * 3;                   // [warp][OG_TT][3]
+  int32_t* sgp = reinterpret_cast<int32_t*>(sacc + OG_WARPS * OG_TT * 3);  // [OG_GCH][8] pair words
+  int32_t* sgo = sgp + OG_GCH * 8;                     // [OG_GCH] offsets
   const int64_t NF = gridDim.x / ntile;
   const int64_t f = blockIdx.x / ntile;
   const int tile = blockIdx.x % ntile;
@@ -537,36 +540,72 @@ __global__ void __launch_bounds__(OG_WARPS * 32)
   const double2* ubf = ub + f * nq * R;
   for (int i = tid; i < ns * 3; i += bd) sU[i] = ubf[(int64_t)tile_src[s0 + i / 3] * 3 + i % 3];
   for (int i = tid; i < OG_WARPS * OG_TT * 3; i += bd) sacc[i] = make_double2(0.0, 0.0);
-  __syncthreads();
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
-  const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
-  double2* myacc = sacc + warp * OG_TT * 3;
-  // this lane's fixed A/B fragment coordinates: row g = (a, re|im), k = 4 ks + tq = (e, re|im)
+  double* accd = reinterpret_cast<double*>(sacc + warp * OG_TT * 3);
+  // this lane's fixed fragment coordinates: row g = (a, re|im); k = 4 ks + tq = (e, re|im)
   const int ra = g >> 1, rr = g & 1;
-  for (int gi = g0 + warp; gi < g1; gi += OG_WARPS) {
-    const int o = grp_o[gi];
-    const int pw = grp_pairs[gi * 8 + g];  // column g of the B fragment: (t_local << 16) | source
-    double c0 = 0.0, c1 = 0.0;
+  const int e0 = tq >> 1, e1 = (4 + tq) >> 1, kc = tq & 1;  // ks = 0, 1 (k & 1 == tq & 1)
+  int sy0 = 0, sy1 = 0;
+  if (ra < 3) {
+    const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+    sy0 = sym[ra][e0];
+    sy1 = e1 < 3 ? sym[ra][e1] : 0;
+  }
+  for (int gc = g0; gc < g1; gc += OG_GCH) {  // group metadata staged in chunks
+    const int ngc = min(OG_GCH, g1 - gc);
+    __syncthreads();
+    for (int i = tid; i < ngc * 8; i += bd) sgp[i] = grp_pairs[(int64_t)gc * 8 + i];
+    for (int i = tid; i < ngc; i += bd) sgo[i] = grp_o[gc + i];
+    __syncthreads();
+    // two groups per iteration (independent chains for latency hiding)
+    for (int gb = 2 * warp; gb < ngc; gb += 2 * OG_WARPS) {
+      int pw[2], p0[2], p1[2], o[2];
+      double a0[2], a1[2], b0[2], b1[2], c0[2], c1[2];
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int k = 4 * ks + tq, e = k >> 1, kc = k & 1;
-      double a = 0.0, b = 0.0;
-      if (ra < 3 && e < 3) {
-        const double2 T = sT[sym[ra][e] * N_OFFSETS + o];
-        a = rr == 0 ? (kc == 0 ? T.x : -T.y) : (kc == 0 ? T.y : T.x);
+      for (int h = 0; h < 2; ++h) {
+        const int gi = min(gb + h, ngc - 1);
+        const bool ok = gb + h < ngc;
+        o[h] = sgo[gi];
+        pw[h] = ok ? sgp[gi * 8 + g] : -1;  // column g of the B fragment: (t_local << 16) | source
+        p0[h] = ok ? sgp[gi * 8 + 2 * tq] : -1;
+        p1[h] = ok ? sgp[gi * 8 + 2 * tq + 1] : -1;
       }
-      if (pw >= 0 && e < 3) {
-        const double2 U = sU[(pw & 0xffff) * 3 + e];
-        b = kc == 0 ? U.x : U.y;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        a0[h] = a1[h] = b0[h] = b1[h] = c0[h] = c1[h] = 0.0;
+        if (ra < 3) {
+          const double2 T0 = sT[sy0 * N_OFFSETS + o[h]];
+          a0[h] = rr == 0 ? (kc == 0 ? T0.x : -T0.y) : (kc == 0 ? T0.y : T0.x);
+          if (e1 < 3) {
+            const double2 T1 = sT[sy1 * N_OFFSETS + o[h]];
+            a1[h] = rr == 0 ? (kc == 0 ? T1.x : -T1.y) : (kc == 0 ? T1.y : T1.x);
+          }
+        }
+        if (pw[h] >= 0) {
+          const double2* U = sU + (pw[h] & 0xffff) * 3;
+          const double2 U0 = U[e0];
+          b0[h] = kc == 0 ? U0.x : U0.y;
+          if (e1 < 3) {
+            const double2 U1 = U[e1];
+            b1[h] = kc == 0 ? U1.x : U1.y;
+          }
+        }
       }
-      dmma(c0, c1, a, b);
-    }
-    if (ra < 3) {
-      const int p0 = grp_pairs[gi * 8 + 2 * tq], p1 = grp_pairs[gi * 8 + 2 * tq + 1];
-      // lanes g = 2a and 2a + 1 update the re and im words of one entry: 8-B accesses only
-      double* accd = reinterpret_cast<double*>(myacc);
-      if (p0 >= 0) accd[2 * ((p0 >> 16) * 3 + ra) + rr] += c0;
-      if (p1 >= 0) accd[2 * ((p1 >> 16) * 3 + ra) + rr] += c1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        dmma(c0[h], c1[h], a0[h], b0[h]);
+        dmma(c0[h], c1[h], a1[h], b1[h]);
+      }
+      // lanes g = 2a and 2a + 1 update the re and im words of one entry (8-B accesses);
+      // the two groups may share targets: applied one after the other
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (ra < 3) {
+          if (p0[h] >= 0) accd[2 * ((p0[h] >> 16) * 3 + ra) + rr] += c0[h];
+          if (p1[h] >= 0) accd[2 * ((p1[h] >> 16) * 3 + ra) + rr] += c1[h];
+        }
+        __syncwarp();  // one group's read-modify-writes complete before the next group's
+      }
     }
   }
   __syncthreads();
