@@ -709,7 +709,10 @@ void run_m2l_fft(Plan& Pl) {
     if (pairs) {
       const int ntb = (int)((ch.nt + PAIR_THREADS - 1) / PAIR_THREADS);
       const unsigned grid = (unsigned)((int64_t)ntb * Pl.NF);
-      static const bool scalar_pairs = getenv("KAFMM_SCALAR_PAIRS") != nullptr;  // A/B knob (profiles/)
+      // k_m2l_ogroups (tensor-core groups) measured 3.3x slower than the scalar per-pair
+      // kernel on C5 (staging bound: 40M (tile, frequency) CTAs each staging ~60 KB);
+      // kept behind KAFMM_OGROUPS=1 for further work (profiles/r01_C5_pairs_ab.txt)
+      static const bool scalar_pairs = getenv("KAFMM_OGROUPS") == nullptr;
       if (Pl.kml == 1)
         k_m2l_pairs<1><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
                                                              Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
