@@ -481,7 +481,7 @@ kafmm_status kafmm_fft_stats(kafmm_plan plan, int64_t* st) {
     st[2] += ch.npar;
     st[3] += ch.nt;
     st[4] += ch.npairs;
-    st[5] += (plan->m2l_mode == M2L_FFT_PAIRS || (plan->m2l_mode == M2L_FFT && ch.block_fill < FFT_PAIR_FILL)) ? 1 : 0;
+    st[5] += (plan->m2l_mode == M2L_FFT_PAIRS || (plan->m2l_mode == M2L_FFT && ch.block_fill < pair_fill_threshold())) ? 1 : 0;
   }
   st[6] = plan->NF;
   st[7] = plan->fft_budget;

@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(OG_WARPS * 32)
 // host
 // ---------------------------------------------------------------------------
 static bool chunk_uses_pairs(const Plan& Pl, const FftChunk& ch) {
-  return Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < FFT_PAIR_FILL);
+  return Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < pair_fill_threshold());
 }
 
 // transforms per forward CTA: 4 at p <= 10 (measured: C5 -3%, others equal), 1 above;

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include <string>
 #include <vector>
@@ -78,6 +79,11 @@ struct FftChunk {
 // blocks are mostly empty (sparse adaptive trees), per V pair.
 enum M2LMode { M2L_DENSE = 0, M2L_FFT = 1, M2L_FFT_BLOCKS = 2, M2L_FFT_PAIRS = 3 };
 constexpr double FFT_PAIR_FILL = 0.35;  // block fill below which a chunk runs per pair (M2L_FFT)
+// the threshold in use: FFT_PAIR_FILL, or KAFMM_PAIR_FILL from the environment (tuning knob)
+inline double pair_fill_threshold() {
+  static const double v = getenv("KAFMM_PAIR_FILL") ? atof(getenv("KAFMM_PAIR_FILL")) : FFT_PAIR_FILL;
+  return v;
+}
 
 // The work lists the evaluation kernels run over.  For a plan built by
 // kafmm_setup they alias the full lists; kafmm_restrict (multi-GPU, one rank
