@@ -31,7 +31,6 @@ static void free_plan(kafmm_plan_s* P) {
   cudaStreamSynchronize(P->stream);
   if (P->side) cudaStreamSynchronize(P->side);
   if (P->gstream) cudaStreamSynchronize(P->gstream);
-  if (P->aux_stream) cudaStreamSynchronize(P->aux_stream);
   if (P->gexec) cudaGraphExecDestroy(P->gexec);
   for (void* p : P->allocs) cudaFree(p);
   for (auto& e : P->ev)
@@ -40,9 +39,6 @@ static void free_plan(kafmm_plan_s* P) {
     if (e) cudaEventDestroy(e);
   if (P->side) cudaStreamDestroy(P->side);
   if (P->gstream) cudaStreamDestroy(P->gstream);
-  if (P->aux_stream) cudaStreamDestroy(P->aux_stream);
-  if (P->ev_aux_in) cudaEventDestroy(P->ev_aux_in);
-  if (P->ev_aux_out) cudaEventDestroy(P->ev_aux_out);
   if (P->ev_gin) cudaEventDestroy(P->ev_gin);
   if (P->ev_gout) cudaEventDestroy(P->ev_gout);
   if (P->ev_near_in) cudaEventDestroy(P->ev_near_in);

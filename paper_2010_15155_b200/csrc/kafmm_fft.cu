@@ -700,49 +700,9 @@ bool fft_supported_p(int p) { return (p >= 3 && p <= 8) || p == 10 || p == 12; }
 
 constexpr int NT_L = 4, NT_G = 2;  // parent n-tiles per warp (Laplace, Stokes family); measured best (profiles/)
 
-static void run_chunk(Plan& Pl, const FftChunk& ch);
-
-// Chunks marked `aux` (small ones, e.g. the coarse levels) run on a third stream
-// with their own spectra buffers, concurrently with the big chunks on the plan's
-// stream; chunks write disjoint target boxes of CHK.  Stage timing mode 1 keeps
-// everything on the plan's stream.
 void run_m2l_fft(Plan& Pl) {
-  const bool aux = Pl.aux_stream != nullptr && Pl.d_ub2 != nullptr && Pl.timing != 1;
-  bool ran_aux = false;
-  if (aux) {
-    KF_CUDA(cudaEventRecord(Pl.ev_aux_in, Pl.stream));
-    KF_CUDA(cudaStreamWaitEvent(Pl.aux_stream, Pl.ev_aux_in, 0));
-    cudaStream_t s0 = Pl.stream;
-    double2 *ub0 = Pl.d_ub, *cb0 = Pl.d_cb;
-    Pl.stream = Pl.aux_stream;
-    Pl.d_ub = Pl.d_ub2;
-    Pl.d_cb = Pl.d_cb2;
-    try {
-      for (const FftChunk& ch : Pl.fft_chunks)
-        if (ch.aux) {
-          run_chunk(Pl, ch);
-          ran_aux = true;
-        }
-    } catch (...) {
-      Pl.stream = s0;
-      Pl.d_ub = ub0;
-      Pl.d_cb = cb0;
-      throw;
-    }
-    Pl.stream = s0;
-    Pl.d_ub = ub0;
-    Pl.d_cb = cb0;
-    KF_CUDA(cudaEventRecord(Pl.ev_aux_out, Pl.aux_stream));
-  }
-  for (const FftChunk& ch : Pl.fft_chunks)
-    if (!aux || !ch.aux) run_chunk(Pl, ch);
-  if (aux) KF_CUDA(cudaStreamWaitEvent(Pl.stream, Pl.ev_aux_out, 0));
-  (void)ran_aux;
-}
-
-static void run_chunk(Plan& Pl, const FftChunk& ch) {
-  {
-    if (ch.nt == 0 || ch.nq == 0) return;
+  for (const FftChunk& ch : Pl.fft_chunks) {
+    if (ch.nt == 0 || ch.nq == 0) continue;
     KF_FFT_DISPATCH(launch_fwd);
     const bool pairs = chunk_uses_pairs(Pl, ch);
     prod_mark(Pl);
@@ -1143,34 +1103,6 @@ void build_fft_chunks(Plan& P, int64_t budget) {
       P.fft_max_npar = std::max(P.fft_max_npar, ch.npar);
       P.fft_chunks.push_back(ch);
       i0 = i1;
-    }
-  }
-  // small chunks (<= 1/16 of the largest's spectra) run concurrently on the aux stream
-  {
-    int64_t big = 0, mq = 0, mp = 0;
-    for (const FftChunk& ch : P.fft_chunks) big = std::max(big, ch.nq + ch.npar);
-    P.fft_max_nq = P.fft_max_npar = 0;
-    for (FftChunk& ch : P.fft_chunks) {
-      ch.aux = (ch.nq + ch.npar) * 16 <= big && P.fft_chunks.size() > 1;
-      if (ch.aux) {
-        mq = std::max(mq, ch.nq);
-        mp = std::max(mp, ch.npar);
-      }
-      // main buffers hold any chunk (timing mode 1 runs the aux chunks there too)
-      P.fft_max_nq = std::max(P.fft_max_nq, ch.nq);
-      P.fft_max_npar = std::max(P.fft_max_npar, ch.npar);
-    }
-    dfree(P, P.d_ub2);
-    dfree(P, P.d_cb2);
-    P.d_ub2 = P.d_cb2 = nullptr;
-    if (mq > 0) {
-      P.d_ub2 = dalloc<double2>(P, (size_t)mq * R * P.NF);
-      P.d_cb2 = dalloc<double2>(P, (size_t)std::max<int64_t>(1, mp) * R * P.NF);
-    }
-    if (!P.aux_stream) {
-      KF_CUDA(cudaStreamCreateWithFlags(&P.aux_stream, cudaStreamNonBlocking));
-      KF_CUDA(cudaEventCreateWithFlags(&P.ev_aux_in, cudaEventDisableTiming));
-      KF_CUDA(cudaEventCreateWithFlags(&P.ev_aux_out, cudaEventDisableTiming));
     }
   }
   dfree(P, P.d_ub);

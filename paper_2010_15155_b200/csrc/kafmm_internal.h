@@ -67,7 +67,6 @@ struct FftChunk {
   int64_t* d_pl_off = nullptr;  // nt + 1
   int32_t* d_pl = nullptr;      // npairs
   double block_fill = 1.0;      // V pairs / (8x8 child blocks the DMMA product runs)
-  bool aux = false;             // small chunk: runs on the aux stream with its own buffers
   // offset-grouped tiles of the sparse Stokes-family product (k_m2l_ogroups)
   int ntile = 0;
   int32_t *d_og_t0 = nullptr, *d_og_soff = nullptr, *d_og_src = nullptr, *d_og_goff = nullptr;
@@ -200,9 +199,6 @@ struct Plan {
   std::vector<FftChunk> fft_chunks;
   double2* d_ub = nullptr;         // [NF][nq][8 kml] source spectra by parent block
   double2* d_cb = nullptr;         // [npar][8 kml][NF] target check spectra, target-major (contiguous per target)
-  double2 *d_ub2 = nullptr, *d_cb2 = nullptr;  // buffers of the aux (small) chunks
-  cudaStream_t aux_stream = nullptr;
-  cudaEvent_t ev_aux_in = nullptr, ev_aux_out = nullptr;
   int64_t fft_max_nq = 0, fft_max_npar = 0, fft_budget = 0;
 
   Jobs J;
