@@ -152,3 +152,19 @@ def test_cuda_graph_replay_matches_and_follows_inputs():
     b = torch.from_numpy(v1).cuda()         # new pointer: re-captured
     assert F.rel_l2(plan.eval(b).cpu().numpy(), ref1) < 1e-12
     plan.set_graph(False)
+
+
+@pytest.mark.parametrize("p", [2, 3, 9, 11])
+def test_orders_outside_the_fft_set_and_tiny_orders(p):
+    # p = 3 uses the FFT M2L (NG = 5); p = 2, 9, 11 fall back to the dense M2L
+    import torch
+    from paper_2010_15155_b200 import KAFMM
+    pts = np.random.default_rng(20 + p).random((3000, 3))
+    kernel = "stokeslet" if p <= 3 else "laplace_pgrad"   # dense Stokes operators at p = 11: 8 GB
+    vals = WL.random_values(kernel, 3000, 21)
+    plan = KAFMM(pts, kernel, p, 30)
+    assert plan.m2l() == ("fft" if p == 3 else "dense")
+    out = plan.eval(torch.from_numpy(vals).cuda()).cpu().numpy()
+    ref = F.fmm(pts, vals, kernel, p, 30)["out"]
+    for lo, hi in F.blocks(kernel):
+        assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10
