@@ -502,127 +502,6 @@ __global__ void __launch_bounds__(PAIR_THREADS)
   for (int a = 0; a < KML; ++a) o[(int64_t)a * NF] = acc[a];
 }
 
-// The per-pair product for sparse Stokes-family chunks on the FP64 tensor
-// cores.  A tile of up to OG_TT targets is handled per (tile, frequency): its
-// V pairs are grouped by offset o (a target has at most one source per
-// offset, so a group's 8 columns are 8 distinct targets), and a group of <= 8
-// pairs is one real GEMM C[6 x 8] = A_o[6 x 6] B[6 x 8] padded to two
-// DMMA.8x8x4 (rows/cols: component x re|im; A = the 2x2 real blocks of the
-// operator spectrum T_o(f), B = the sources' spectra).  The tile's source
-// spectra and the frequency's operator spectra are staged in shared memory;
-// each warp accumulates into its own copy of the tile's outputs (no atomics:
-// within a warp the columns of a group are distinct targets), summed at the end.
-constexpr int OG_TT = 64, OG_NSMAX = 512, OG_WARPS = 4, OG_GCH = 256;
-constexpr size_t OG_SMEM = (size_t)(6 * N_OFFSETS + OG_NSMAX * 3 + OG_WARPS * OG_TT * 3) * sizeof(double2) +
-                           (size_t)OG_GCH * (8 * sizeof(int32_t) + sizeof(int32_t));
-
-__global__ void __launch_bounds__(OG_WARPS * 32)
-    k_m2l_ogroups(int64_t nq, int64_t npar, int ntile, const double2* __restrict__ that,
-                  const double2* __restrict__ ub, double2* __restrict__ cb, const int2* __restrict__ tpb,
-                  const int32_t* __restrict__ tile_t0, const int32_t* __restrict__ tile_soff,
-                  const int32_t* __restrict__ tile_src, const int32_t* __restrict__ tile_goff,
-                  const int16_t* __restrict__ grp_o, const int32_t* __restrict__ grp_pairs) {
-  constexpr int R = 24;
-  extern __shared__ __align__(16) double2 og[];
-  double2* sT = og;                                    // [6][316] planar
-  double2* sU = sT + 6 * N_OFFSETS;                    // [ns][3]
-  double2* sacc = sU + OG_NSMAX * 3;                   // [warp][OG_TT][3]
-  int32_t* sgp = reinterpret_cast<int32_t*>(sacc + OG_WARPS * OG_TT * 3);  // [OG_GCH][8] pair words
-  int32_t* sgo = sgp + OG_GCH * 8;                     // [OG_GCH] offsets
-  const int64_t NF = gridDim.x / ntile;
-  const int64_t f = blockIdx.x / ntile;
-  const int tile = blockIdx.x % ntile;
-  const int tid = threadIdx.x, bd = blockDim.x;
-  const int t0 = tile_t0[tile], nt = tile_t0[tile + 1] - t0;
-  const int s0 = tile_soff[tile], ns = tile_soff[tile + 1] - s0;
-  const int g0 = tile_goff[tile], g1 = tile_goff[tile + 1];
-  for (int i = tid; i < N_OFFSETS * 6; i += bd) sT[(i % 6) * N_OFFSETS + i / 6] = that[f * N_OFFSETS * 6 + i];
-  const double2* ubf = ub + f * nq * R;
-  for (int i = tid; i < ns * 3; i += bd) sU[i] = ubf[(int64_t)tile_src[s0 + i / 3] * 3 + i % 3];
-  for (int i = tid; i < OG_WARPS * OG_TT * 3; i += bd) sacc[i] = make_double2(0.0, 0.0);
-  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
-  double* accd = reinterpret_cast<double*>(sacc + warp * OG_TT * 3);
-  // this lane's fixed fragment coordinates: row g = (a, re|im); k = 4 ks + tq = (e, re|im)
-  const int ra = g >> 1, rr = g & 1;
-  const int e0 = tq >> 1, e1 = (4 + tq) >> 1, kc = tq & 1;  // ks = 0, 1 (k & 1 == tq & 1)
-  int sy0 = 0, sy1 = 0;
-  if (ra < 3) {
-    const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
-    sy0 = sym[ra][e0];
-    sy1 = e1 < 3 ? sym[ra][e1] : 0;
-  }
-  for (int gc = g0; gc < g1; gc += OG_GCH) {  // group metadata staged in chunks
-    const int ngc = min(OG_GCH, g1 - gc);
-    __syncthreads();
-    for (int i = tid; i < ngc * 8; i += bd) sgp[i] = grp_pairs[(int64_t)gc * 8 + i];
-    for (int i = tid; i < ngc; i += bd) sgo[i] = grp_o[gc + i];
-    __syncthreads();
-    // two groups per iteration (independent chains for latency hiding)
-    for (int gb = 2 * warp; gb < ngc; gb += 2 * OG_WARPS) {
-      int pw[2], p0[2], p1[2], o[2];
-      double a0[2], a1[2], b0[2], b1[2], c0[2], c1[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int gi = min(gb + h, ngc - 1);
-        const bool ok = gb + h < ngc;
-        o[h] = sgo[gi];
-        pw[h] = ok ? sgp[gi * 8 + g] : -1;  // column g of the B fragment: (t_local << 16) | source
-        p0[h] = ok ? sgp[gi * 8 + 2 * tq] : -1;
-        p1[h] = ok ? sgp[gi * 8 + 2 * tq + 1] : -1;
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        a0[h] = a1[h] = b0[h] = b1[h] = c0[h] = c1[h] = 0.0;
-        if (ra < 3) {
-          const double2 T0 = sT[sy0 * N_OFFSETS + o[h]];
-          a0[h] = rr == 0 ? (kc == 0 ? T0.x : -T0.y) : (kc == 0 ? T0.y : T0.x);
-          if (e1 < 3) {
-            const double2 T1 = sT[sy1 * N_OFFSETS + o[h]];
-            a1[h] = rr == 0 ? (kc == 0 ? T1.x : -T1.y) : (kc == 0 ? T1.y : T1.x);
-          }
-        }
-        if (pw[h] >= 0) {
-          const double2* U = sU + (pw[h] & 0xffff) * 3;
-          const double2 U0 = U[e0];
-          b0[h] = kc == 0 ? U0.x : U0.y;
-          if (e1 < 3) {
-            const double2 U1 = U[e1];
-            b1[h] = kc == 0 ? U1.x : U1.y;
-          }
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        dmma(c0[h], c1[h], a0[h], b0[h]);
-        dmma(c0[h], c1[h], a1[h], b1[h]);
-      }
-      // lanes g = 2a and 2a + 1 update the re and im words of one entry (8-B accesses);
-      // the two groups may share targets: applied one after the other
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (ra < 3) {
-          if (p0[h] >= 0) accd[2 * ((p0[h] >> 16) * 3 + ra) + rr] += c0[h];
-          if (p1[h] >= 0) accd[2 * ((p1[h] >> 16) * 3 + ra) + rr] += c1[h];
-        }
-        __syncwarp();  // one group's read-modify-writes complete before the next group's
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < nt * 3; i += bd) {
-    double2 v = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int w = 0; w < OG_WARPS; ++w) {
-      const double2 x = sacc[w * OG_TT * 3 + i];
-      v.x += x.x;
-      v.y += x.y;
-    }
-    const int t = t0 + i / 3, a = i % 3;
-    const int2 pb = tpb[t];
-    cb[((int64_t)pb.x * R + pb.y * 3 + a) * NF + f] = v;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // host
 // ---------------------------------------------------------------------------
@@ -709,26 +588,14 @@ void run_m2l_fft(Plan& Pl) {
     if (pairs) {
       const int ntb = (int)((ch.nt + PAIR_THREADS - 1) / PAIR_THREADS);
       const unsigned grid = (unsigned)((int64_t)ntb * Pl.NF);
-      // k_m2l_ogroups (tensor-core groups) measured 3.3x slower than the scalar per-pair
-      // kernel on C5 (staging bound: 40M (tile, frequency) CTAs each staging ~60 KB);
-      // kept behind KAFMM_OGROUPS=1 for further work (profiles/r01_C5_pairs_ab.txt)
-      static const bool scalar_pairs = getenv("KAFMM_OGROUPS") == nullptr;
+      // (a tensor-core variant that grouped a tile's pairs by offset measured 3.3x slower
+      // on C5, staging bound: profiles/r01_C5_pairs_ab.txt; removed after round 1)
       if (Pl.kml == 1)
         k_m2l_pairs<1><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
                                                              Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
-      else if (scalar_pairs || ch.ntile == 0)
+      else
         k_m2l_pairs<3><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
                                                              Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
-      else {
-        static bool attr = false;
-        if (!attr) {
-          KF_CUDA(cudaFuncSetAttribute(k_m2l_ogroups, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OG_SMEM));
-          attr = true;
-        }
-        k_m2l_ogroups<<<(unsigned)((int64_t)ch.ntile * Pl.NF), OG_WARPS * 32, OG_SMEM, Pl.stream>>>(
-            ch.nq, ch.npar, ch.ntile, Pl.d_that, Pl.d_ub, Pl.d_cb, ch.d_tpb, ch.d_og_t0, ch.d_og_soff, ch.d_og_src,
-            ch.d_og_goff, ch.d_og_o, ch.d_og_pairs);
-      }
     } else {
       // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
       // (fewer registers, more resident warps) -- a tuning knob measured in profiles/
@@ -1023,60 +890,6 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         int64_t blocks = 0;
         for (int32_t v : nb) blocks += v >= 0;
         ch.block_fill = blocks ? (double)ch.npairs / (64.0 * (double)blocks) : 1.0;
-      }
-      if (P.kml == 3) {
-        // offset-grouped tiles for k_m2l_ogroups: up to OG_TT consecutive targets whose
-        // distinct sources fit OG_NSMAX; pairs sorted by offset, runs cut into groups of 8
-        std::vector<int32_t> t0v(1, 0), soff(1, 0), srcs, goff(1, 0), gp;
-        std::vector<int16_t> go;
-        std::vector<int32_t> mark(std::max<int64_t>(1, (int64_t)qs.size() * 8), -1);
-        std::vector<int64_t> rec;  // (oid << 32) | (t_local << 16) | local source
-        size_t t = 0;
-        while (t < tb.size()) {
-          const size_t ts = t;
-          std::vector<int32_t> tsrc;
-          while (t < tb.size() && (int)(t - ts) < OG_TT) {
-            int add = 0;
-            for (int64_t e = ploff[t]; e < ploff[t + 1]; ++e) add += mark[pl[e] >> 9] < 0;
-            if (t > ts && (int)tsrc.size() + add > OG_NSMAX) break;
-            for (int64_t e = ploff[t]; e < ploff[t + 1]; ++e) {
-              const int32_t qc = pl[e] >> 9;
-              if (mark[qc] < 0) {
-                mark[qc] = (int32_t)tsrc.size();
-                tsrc.push_back(qc);
-              }
-            }
-            ++t;
-          }
-          if ((int)tsrc.size() > OG_NSMAX) throw Error{KAFMM_ECUDA, "FFT M2L: a target with more V sources than a tile holds"};
-          rec.clear();
-          for (size_t u = ts; u < t; ++u)
-            for (int64_t e = ploff[u]; e < ploff[u + 1]; ++e)
-              rec.push_back(((int64_t)(pl[e] & 511) << 32) | ((int64_t)(u - ts) << 16) | mark[pl[e] >> 9]);
-          std::sort(rec.begin(), rec.end());
-          size_t i = 0;
-          while (i < rec.size()) {
-            const int o = (int)(rec[i] >> 32);
-            go.push_back((int16_t)o);
-            int k = 0;
-            for (; k < 8 && i < rec.size() && (int)(rec[i] >> 32) == o; ++k, ++i) gp.push_back((int32_t)(rec[i] & 0xffffffff));
-            for (; k < 8; ++k) gp.push_back(-1);
-          }
-          for (int32_t qc : tsrc) {
-            srcs.push_back(qc);
-            mark[qc] = -1;
-          }
-          t0v.push_back((int32_t)t);
-          soff.push_back((int32_t)srcs.size());
-          goff.push_back((int32_t)go.size());
-        }
-        ch.ntile = (int)(t0v.size() - 1);
-        ch.d_og_t0 = h2d_vec(P, t0v);
-        ch.d_og_soff = h2d_vec(P, soff);
-        ch.d_og_src = h2d_vec(P, srcs);
-        ch.d_og_goff = h2d_vec(P, goff);
-        ch.d_og_o = h2d_vec(P, go);
-        ch.d_og_pairs = h2d_vec(P, gp);
       }
       ch.d_tpb_pair = dalloc<int2>(P, std::max<size_t>(1, tpb_pair.size()));
       if (!tpb_pair.empty())

@@ -67,11 +67,6 @@ struct FftChunk {
   int64_t* d_pl_off = nullptr;  // nt + 1
   int32_t* d_pl = nullptr;      // npairs
   double block_fill = 1.0;      // V pairs / (8x8 child blocks the DMMA product runs)
-  // offset-grouped tiles of the sparse Stokes-family product (k_m2l_ogroups)
-  int ntile = 0;
-  int32_t *d_og_t0 = nullptr, *d_og_soff = nullptr, *d_og_src = nullptr, *d_og_goff = nullptr;
-  int16_t* d_og_o = nullptr;
-  int32_t* d_og_pairs = nullptr;
 };
 
 // M2L variants: dense per-offset GEMMs, or the FFT lattice convolution whose
