@@ -109,6 +109,19 @@ kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_o
  *   trg_out     host, n x k_t */
 kafmm_status kafmm_eval_host(kafmm_plan plan, const double* src_values, double* trg_out);
 
+/* Separate source and target point sets (STKFMM takes SL
+ * and target points as different sets).  The octree is built on the union
+ * [sources; targets]; targets carry zero source strength and only the target
+ * rows are returned, so the result is sum over sources of K(x_t, y_s) s_s,
+ * with pairs at r^2 == 0 skipped by the singular kernels as usual.
+ *   src_points  device, n_src x 3;  trg_points  device, n_trg x 3 (both in [0,1)^3)
+ *   kafmm_eval2: src_values device n_src x k_s, trg_out device n_trg x k_t.
+ * kafmm_eval on such a plan is EINVAL-free but works on the union rows; use
+ * kafmm_eval2.  ESTATE if kafmm_eval2 is called on a plan from kafmm_setup. */
+kafmm_status kafmm_setup2(const double* src_points, int64_t n_src, const double* trg_points, int64_t n_trg,
+                          int kernel, int p, int max_pts_per_leaf, kafmm_plan* out);
+kafmm_status kafmm_eval2(kafmm_plan plan, const double* src_values, double* trg_out);
+
 /* Validate source values (finite; b / eps >= 0) on the device.  Synchronous.
  * kafmm_eval itself does not check, to keep the hot path free of host syncs. */
 kafmm_status kafmm_check_values(kafmm_plan plan, const double* src_values);

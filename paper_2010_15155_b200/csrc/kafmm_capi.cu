@@ -218,6 +218,58 @@ kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_o
   KF_API_END
 }
 
+kafmm_status kafmm_setup2(const double* src_points, int64_t n_src, const double* trg_points, int64_t n_trg,
+                          int kernel, int p, int max_pts_per_leaf, kafmm_plan* out) {
+  if (out) *out = nullptr;
+  if (!src_points || !trg_points || !out || n_src < 1 || n_trg < 1 || n_src + n_trg > INT32_MAX) {
+    set_error("kafmm_setup2: invalid argument");
+    return KAFMM_EINVAL;
+  }
+  double* u = nullptr;
+  if (cudaMalloc(&u, (size_t)(n_src + n_trg) * 3 * 8) != cudaSuccess) {
+    set_error("kafmm_setup2: out of memory");
+    return KAFMM_ENOMEM;
+  }
+  cudaMemcpy(u, src_points, (size_t)n_src * 24, cudaMemcpyDeviceToDevice);
+  cudaMemcpy(u + 3 * n_src, trg_points, (size_t)n_trg * 24, cudaMemcpyDeviceToDevice);
+  kafmm_status st = kafmm_setup(u, n_src + n_trg, kernel, p, max_pts_per_leaf, out);
+  cudaFree(u);
+  if (st != KAFMM_OK) return st;
+  Plan& P = **out;
+  try {
+    P.n_src = n_src;
+    P.d_uvals = dalloc<double>(P, (size_t)P.n * P.ks);  // zero (dalloc clears): target rows stay 0
+    P.d_uout = dalloc<double>(P, (size_t)P.n * P.kt);
+    KF_CUDA(cudaStreamSynchronize(P.stream));
+  } catch (const Error& e) {
+    set_error(e.msg);
+    kafmm_destroy(*out);
+    *out = nullptr;
+    return e.st;
+  }
+  return KAFMM_OK;
+}
+
+kafmm_status kafmm_eval2(kafmm_plan plan, const double* src_values, double* trg_out) {
+  if (!plan || !src_values || !trg_out) {
+    set_error("kafmm_eval2: null argument");
+    return KAFMM_EINVAL;
+  }
+  if (plan->n_src < 0) {
+    set_error("kafmm_eval2: plan not made by kafmm_setup2");
+    return KAFMM_ESTATE;
+  }
+  KF_API_BEGIN
+  Plan& P = *plan;
+  KF_CUDA(cudaMemcpyAsync(P.d_uvals, src_values, (size_t)P.n_src * P.ks * 8, cudaMemcpyDeviceToDevice, P.stream));
+  run_eval(P, P.d_uvals, P.d_uout);
+  collect_stage_times(P);
+  KF_CUDA(cudaMemcpyAsync(trg_out, P.d_uout + (size_t)P.n_src * P.kt, (size_t)(P.n - P.n_src) * P.kt * 8,
+                          cudaMemcpyDeviceToDevice, P.stream));
+  return KAFMM_OK;
+  KF_API_END
+}
+
 kafmm_status kafmm_set_graph(kafmm_plan plan, int on) {
   if (!plan) return KAFMM_EINVAL;
   plan->use_graph = on != 0;

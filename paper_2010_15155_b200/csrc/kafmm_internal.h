@@ -198,6 +198,10 @@ struct Plan {
 
   Jobs J;
   bool restricted = false;
+  // kafmm_setup2: rows [0, n_src) of the union are sources, the rest targets
+  int64_t n_src = -1;
+  double* d_uvals = nullptr;   // union source values (target rows stay zero)
+  double* d_uout = nullptr;    // union outputs
 
   // GEMM batches
   GemmBatch g_uc2ue_1, g_uc2ue_2;              // S2M leaves (level >= 2)

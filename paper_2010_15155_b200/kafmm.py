@@ -66,6 +66,9 @@ _SIGS = [
     ("kafmm_get_m2l_mode", C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     ("kafmm_fft_stats", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kafmm_set_graph", C.c_int, [C.c_void_p, C.c_int]),
+    ("kafmm_setup2", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int,
+                               C.POINTER(C.c_void_p)]),
+    ("kafmm_eval2", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("kafmm_restrict", C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
     ("kafmm_eval_up", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kafmm_eval_down", C.c_int, [C.c_void_p, C.c_void_p]),
@@ -326,3 +329,35 @@ class KAFMMWall:
 
     def close(self):
         self.__del__()
+
+
+class KAFMM2(KAFMM):
+    """Separate source and target point sets (kafmm_setup2 / kafmm_eval2):
+    eval(src_values (n_src x k_s)) -> (n_trg x k_t) at the target points."""
+
+    def __init__(self, src_points, trg_points, kernel: str, p: int, max_pts: int, stream=None):
+        torch = _torch()
+        self.lib = load_library()
+        self.kernel = kernel
+        dev = lambda a: (torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()  # noqa: E731
+                         if isinstance(a, np.ndarray) else a.to(device="cuda", dtype=torch.float64).contiguous())
+        sp, tp = dev(src_points), dev(trg_points)
+        self.n_src, self.n_trg = int(sp.shape[0]), int(tp.shape[0])
+        self.n = self.n_src + self.n_trg
+        self.k_s, self.k_t = kernel_dims(kernel)
+        h = C.c_void_p()
+        torch.cuda.synchronize()
+        _check(self.lib.kafmm_setup2(C.c_void_p(sp.data_ptr()), self.n_src, C.c_void_p(tp.data_ptr()), self.n_trg,
+                                     KERNELS[kernel], int(p), int(max_pts), C.byref(h)), "kafmm_setup2")
+        self.h = h
+        if stream is not None:
+            self.set_stream(stream)
+
+    def eval(self, src, out=None):
+        torch = _torch()
+        assert src.is_cuda and src.dtype == torch.float64 and src.shape == (self.n_src, self.k_s)
+        src = src.contiguous()
+        if out is None:
+            out = torch.empty((self.n_trg, self.k_t), dtype=torch.float64, device=src.device)
+        _check(self.lib.kafmm_eval2(self.h, C.c_void_p(src.data_ptr()), C.c_void_p(out.data_ptr())), "kafmm_eval2")
+        return out

@@ -168,3 +168,21 @@ def test_orders_outside_the_fft_set_and_tiny_orders(p):
     ref = F.fmm(pts, vals, kernel, p, 30)["out"]
     for lo, hi in F.blocks(kernel):
         assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10
+
+
+@pytest.mark.parametrize("kernel", ["laplace_pgrad", "stokes_reg_vel_omega"])
+def test_separate_source_and_target_sets(kernel):
+    import torch
+    from paper_2010_15155_b200 import KAFMM2
+    rng = np.random.default_rng(43)
+    src = rng.random((4000, 3))
+    trg = np.concatenate([0.2 + 0.5 * rng.random((2500, 3)), src[:100]])  # some targets on sources
+    vals = WL.random_values(kernel, 4000, 44)
+    plan = KAFMM2(src, trg, kernel, 6, 32)
+    out = plan.eval(torch.from_numpy(vals).cuda()).cpu().numpy()
+    assert out.shape == (trg.shape[0], WL.KERNEL_DIMS[kernel][1])
+    union = np.concatenate([src, trg])
+    uv = np.concatenate([vals, np.zeros((trg.shape[0], vals.shape[1]))])
+    ref = F.fmm(union, uv, kernel, 6, 32)["out"][4000:]
+    for lo, hi in F.blocks(kernel):
+        assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10

@@ -156,3 +156,19 @@ def test_polydisperse_lognormal_error_decreases_with_p(cid):
         errs.append(max(F.rel_l2(out[:, lo:hi], d[:, lo:hi]) for lo, hi in F.blocks(spec.kernel)))
     for e0, e1 in zip(errs, errs[1:]):
         assert e1 < e0 / 10.0, errs
+
+
+def test_separate_source_and_target_sets_by_union():
+    # sources and targets may be different point sets.  The FMM over
+    # the union with zero strength on the targets, read at the target rows, is the
+    # sum over sources only (checked against the O1 direct sum from the sources)
+    rng = np.random.default_rng(41)
+    src = rng.random((900, 3))
+    trg = 0.3 + 0.4 * rng.random((500, 3))
+    vals = WL.random_values("stokeslet", 900, 42)
+    union = np.concatenate([src, trg])
+    uv = np.concatenate([vals, np.zeros((500, 3))])
+    out = F.fmm(union, uv, "stokeslet", 8, 30)["out"][900:]
+    from oracle.kernels import direct_sum
+    d = direct_sum("G", trg, src, vals)
+    assert F.rel_l2(out, d) < 1e-5
