@@ -218,6 +218,14 @@ kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_o
   KF_API_END
 }
 
+// Target rows of the union carry zero strength; for the regularised Stokes
+// kernels their blob size is set to 1 so that a target coinciding with another
+// point gives 0 * finite instead of 0 * (1/0) (reading R19).
+__global__ void k_fill_col(double* v, int64_t lo, int64_t hi, int ks, int col, double x) {
+  int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < hi) v[i * ks + col] = x;
+}
+
 kafmm_status kafmm_setup2(const double* src_points, int64_t n_src, const double* trg_points, int64_t n_trg,
                           int kernel, int p, int max_pts_per_leaf, kafmm_plan* out) {
   if (out) *out = nullptr;
@@ -240,6 +248,11 @@ kafmm_status kafmm_setup2(const double* src_points, int64_t n_src, const double*
     P.n_src = n_src;
     P.d_uvals = dalloc<double>(P, (size_t)P.n * P.ks);  // zero (dalloc clears): target rows stay 0
     P.d_uout = dalloc<double>(P, (size_t)P.n * P.kt);
+    const int pcol = kernel == KAFMM_STOKES_REG_VEL ? 3 : kernel == KAFMM_STOKES_REG_VEL_OMEGA ? 6 : -1;
+    if (pcol >= 0) {
+      k_fill_col<<<(unsigned)((n_trg + 255) / 256), 256, 0, P.stream>>>(P.d_uvals, n_src, P.n, P.ks, pcol, 1.0);
+      KF_CHECK_LAUNCH();
+    }
     KF_CUDA(cudaStreamSynchronize(P.stream));
   } catch (const Error& e) {
     set_error(e.msg);

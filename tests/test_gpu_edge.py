@@ -170,7 +170,7 @@ def test_orders_outside_the_fft_set_and_tiny_orders(p):
         assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10
 
 
-@pytest.mark.parametrize("kernel", ["laplace_pgrad", "stokes_reg_vel_omega"])
+@pytest.mark.parametrize("kernel", ["laplace_pgrad", "stokes_reg_vel_omega", "rpy"])
 def test_separate_source_and_target_sets(kernel):
     import torch
     from paper_2010_15155_b200 import KAFMM2
@@ -183,6 +183,8 @@ def test_separate_source_and_target_sets(kernel):
     assert out.shape == (trg.shape[0], WL.KERNEL_DIMS[kernel][1])
     union = np.concatenate([src, trg])
     uv = np.concatenate([vals, np.zeros((trg.shape[0], vals.shape[1]))])
+    if kernel in WL.PARAM_COL and kernel != "rpy":
+        uv[4000:, WL.PARAM_COL[kernel]] = 1.0   # reading R19: blob size of zero-strength target rows
     ref = F.fmm(union, uv, kernel, 6, 32)["out"][4000:]
     for lo, hi in F.blocks(kernel):
         assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10
