@@ -352,7 +352,11 @@ __global__ void __launch_bounds__(256)
 // parents; the A fragments are gathered from the frequency's operator spectra
 // in shared memory through a precomputed index table, the B fragments are the
 // colleagues' child blocks (one 16-B load per lane), and a complex product is
-// four DMMA.8x8x4 (re re, -im im, re im, im re).
+// three DMMA.8x8x4 (Gauss / Karatsuba): with A = a + ib, B = c + id,
+//     P1 = sum a c,  P2 = sum b d,  P3 = sum (a + b)(c + d),
+//     Re = P1 - P2,  Im = P3 - P1 - P2,
+// the sums a + b and c + d formed in registers (one DADD per fragment),
+// the three accumulators combined once in the epilogue.
 constexpr int DM_WARPS = 4;
 
 template <int KML, int NT>
@@ -370,11 +374,13 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
   const int g = lane >> 2, tq = lane & 3;
   const int64_t P0 = ((int64_t)pb * DM_WARPS + warp) * PPW;
   if (P0 >= npar) return;
-  double acc[KML][NT][2][2];
+  double acc[KML][NT][3][2];  // P1, P2, P3 (see above)
 #pragma unroll
   for (int m = 0; m < KML; ++m)
 #pragma unroll
-    for (int n = 0; n < NT; ++n) acc[m][n][0][0] = acc[m][n][0][1] = acc[m][n][1][0] = acc[m][n][1][1] = 0.0;
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) acc[m][n][k][0] = acc[m][n][k][1] = 0.0;
   const double2* ubf = ub + f * nq * R;
   int qn[NT];  // colleague block of the next direction (prefetched)
 #pragma unroll
@@ -399,24 +405,24 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
     const int16_t* ai_tab = aidx + d * KS * KML * 32 + lane;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      double ar[KML], ai[KML], an[KML];
+      double ar[KML], ai[KML], as[KML];
 #pragma unroll
       for (int m = 0; m < KML; ++m) {
         const int idx = ai_tab[(ks * KML + m) * 32];
         const double2 t = idx >= 0 ? sT[idx] : make_double2(0.0, 0.0);
         ar[m] = t.x;
         ai[m] = t.y;
-        an[m] = -t.y;
+        as[m] = t.x + t.y;
       }
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         const double2 u = qb[n] >= 0 ? ubf[qb[n] + ks * 4] : make_double2(0.0, 0.0);
+        const double us = u.x + u.y;
 #pragma unroll
         for (int m = 0; m < KML; ++m) {
           dmma(acc[m][n][0][0], acc[m][n][0][1], ar[m], u.x);
-          dmma(acc[m][n][0][0], acc[m][n][0][1], an[m], u.y);
-          dmma(acc[m][n][1][0], acc[m][n][1][1], ar[m], u.y);
-          dmma(acc[m][n][1][0], acc[m][n][1][1], ai[m], u.x);
+          dmma(acc[m][n][1][0], acc[m][n][1][1], ai[m], u.y);
+          dmma(acc[m][n][2][0], acc[m][n][2][1], as[m], us);
         }
       }
     }
@@ -429,7 +435,10 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t Pn = P0 + n * 8 + 2 * tq + e;
-        if (Pn < npar) cbf[(Pn * R + m * 8 + g) * NF] = make_double2(acc[m][n][0][e], acc[m][n][1][e]);
+        if (Pn < npar) {
+          const double p1 = acc[m][n][0][e], p2 = acc[m][n][1][e];
+          cbf[(Pn * R + m * 8 + g) * NF] = make_double2(p1 - p2, acc[m][n][2][e] - p1 - p2);
+        }
       }
 }
 
