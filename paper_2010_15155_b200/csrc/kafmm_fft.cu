@@ -359,8 +359,14 @@ __global__ void __launch_bounds__(256)
 // the three accumulators combined once in the epilogue.
 constexpr int DM_WARPS = 4;
 
+#ifndef KF_DMMA_MINB1
+#define KF_DMMA_MINB1 1
+#endif
+#ifndef KF_DMMA_MINB3
+#define KF_DMMA_MINB3 4  // Stokes family: cap 128 registers, 4 CTAs per SM (C3 product -14%, profiles/r01_dmma_ab.txt)
+#endif
 template <int KML, int NT>
-__global__ void __launch_bounds__(DM_WARPS * 32)
+__global__ void __launch_bounds__(DM_WARPS * 32, KML == 1 ? KF_DMMA_MINB1 : KF_DMMA_MINB3)
     k_m2l_dmma(int64_t npar, int64_t nq, int npb, const double2* __restrict__ that, const double2* __restrict__ ub,
                double2* __restrict__ cb, const int32_t* __restrict__ nbr, const int16_t* __restrict__ aidx) {
   constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML, KS = R / 4, PPW = NT * 8;
@@ -586,7 +592,11 @@ static void launch_inv(Plan& Pl, const FftChunk& ch) {
 
 bool fft_supported_p(int p) { return (p >= 3 && p <= 8) || p == 10 || p == 12; }
 
-constexpr int NT_L = 4, NT_G = 2;  // parent n-tiles per warp (Laplace, Stokes family); measured best (profiles/)
+#ifndef KF_NT_L
+#define KF_NT_L 4
+#define KF_NT_G 2
+#endif
+constexpr int NT_L = KF_NT_L, NT_G = KF_NT_G;  // parent n-tiles per warp (Laplace, Stokes family); measured best (profiles/)
 
 void run_m2l_fft(Plan& Pl) {
   for (const FftChunk& ch : Pl.fft_chunks) {

@@ -1,7 +1,7 @@
-set -x
-timeout 600 python -m pytest tests/test_gpu_m2l_modes.py tests/test_gpu_parity.py -x -q > gpurun_out/k_pytest.log 2>&1; echo pytest=$?; tail -2 gpurun_out/k_pytest.log
-for c in 2 3; do
- timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e > gpurun_out/k_c$c.json 2>gpurun_out/k_c$c.err
- KAFMM_DMMA_NT=1 timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e > gpurun_out/k_c${c}_half.json 2>>gpurun_out/k_c$c.err
+# A/B of library variants on C2 and C3 (KAFMM_LIB selects the .so)
+for v in "" m64 nt3 nt6; do
+  lib=paper_2010_15155_b200/libkafmm${v:+_$v}.so
+  for c in 2 3; do
+    KAFMM_LIB=$PWD/$lib timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e > gpurun_out/ab_c${c}_${v:-base}.json 2>gpurun_out/ab_c${c}_${v:-base}.err
+  done
 done
-timeout 400 python bench.py --config 4 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/k_c4.json 2>gpurun_out/k_c4.err
