@@ -89,14 +89,8 @@ __global__ void k_spectra_transpose(int NF, int nc, const double2* __restrict__ 
 template <int P>
 struct FftDims {
   static constexpr int NG = 2 * P - 1, NZ = NG / 2 + 1, NF = NG * NG * NZ;
-  static constexpr int CUBE = (P * P * P + 1) / 2 * 2;  // doubles, keep 16-B alignment after it
-  // DFT-pass fragment table sizes (doubles): forward z, forward y/x, inverse x/y
-  static constexpr int TZ = 32 * ((P + 3) / 4) * ((2 * NZ + 7) / 8);
-  static constexpr int TF = 32 * ((2 * P + 3) / 4) * ((2 * NG + 7) / 8);
-  static constexpr int TI = 32 * ((2 * NG + 3) / 4) * ((2 * P + 7) / 8);
-  static constexpr size_t FWD_SMEM = (CUBE + 2 * (P * P * NZ + P * NG * NZ + NG) + TZ + TF) * sizeof(double);
-  // spectrum column (later reused for the y-pass output) + x-pass output + twiddles + table
-  static constexpr size_t INV_SMEM = (2 * (NF + P * NG * NZ + NG) + TI) * sizeof(double);
+  // inverse: x-pass output [x][fy][fz] + y-pass output [x][y][fz] (complex) + twiddles
+  static constexpr size_t INV_SMEM = (size_t)2 * (P * NG * NZ + P * P * NZ + NG) * sizeof(double);
 };
 
 __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
@@ -128,17 +122,14 @@ struct DftShape {
 };
 
 // fragment tables: [ks][nt][lane] twiddle block entries (host-built, see
-// build_fft_m2l), staged in shared memory by the CTA; a lane reads its own
-// entry right before each DMMA (conflict-free), which keeps the register
-// count low enough for more resident CTAs than holding the table in registers
-__device__ __forceinline__ void stage_table(double* __restrict__ dst, const double* __restrict__ src, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-}
+// build_fft_m2l) in global memory; a lane reads its own entry right before
+// each DMMA (coalesced, L1-resident: every CTA of the launch reads the same
+// few KB), which keeps the register count low and costs no shared memory
 
 // one pass over nlines lines by the CTA's warps; loadA(line, k) -> double,
 // storeC(line, o, double2) for o < nout
 template <int NKS, int NNT, class LoadA, class StoreC>
-__device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __restrict__ wsm, LoadA loadA,
+__device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __restrict__ wtab, LoadA loadA,
                                          StoreC storeC) {
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
@@ -152,7 +143,7 @@ __device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __r
     for (int k = 0; k < NKS; ++k) {
       const double a = ok ? loadA(line, 4 * k + tq) : 0.0;
 #pragma unroll
-      for (int n = 0; n < NNT; ++n) dmma(acc[n][0], acc[n][1], a, wsm[(k * NNT + n) * 32 + lane]);
+      for (int n = 0; n < NNT; ++n) dmma(acc[n][0], acc[n][1], a, __ldg(wtab + (k * NNT + n) * 32 + lane));
     }
     if (ok) {
 #pragma unroll
@@ -169,112 +160,128 @@ __device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __r
 // index.  Each transform: the child's upward equivalent density on the p^3
 // lattice (non-zero on the surface only) -> its real DFT on the NG^3 grid,
 // z (real -> half spectrum), y, x passes on the tensor cores over the lines of
-// all NB transforms at once (transform index fastest, so one frequency's
-// stores are NB consecutive 16-B words).  A missing child's slots are
+// all the group's transforms at once.  The z pass reads the density straight
+// from UE through the lattice -> surface-index map (no dense p^3 cube in
+// shared memory); the x pass has the transform index fastest, so one
+// frequency's stores are consecutive 16-B words.  A missing child's slots are
 // zero-filled when the chunk's product reads parent blocks, else skipped.
 template <int P>
 struct FwdCfg {
   using D = FftDims<P>;
-  static constexpr int PER = D::CUBE + 2 * (P * P * D::NZ + P * D::NG * D::NZ);  // doubles per transform
+  static constexpr int PER = 2 * (P * P * D::NZ + P * D::NG * D::NZ);  // doubles per transform (z, y outputs)
   template <int NB>
-  static constexpr size_t smem() { return (size_t)(NB * PER + D::TZ + D::TF) * sizeof(double); }
+  static constexpr size_t smem() { return (size_t)NB * PER * sizeof(double); }
 };
+
+template <int N, class T>
+__device__ __forceinline__ T pick(const T (&a)[N], int t, int n) {  // a[t] without local memory
+  T r = a[0];
+#pragma unroll
+  for (int j = 1; j < N; ++j)
+    if (j < n && t == j) r = a[j];
+  return r;
+}
+
+template <int P, int NB, int NBC>
+__device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* (&src)[NB], const int (&slot)[NB],
+                                         const int16_t* __restrict__ lmap, int kml, double2* __restrict__ ub,
+                                         int64_t nq, int64_t q, int R, const double* __restrict__ wz,
+                                         const double* __restrict__ wf) {
+  using D = FftDims<P>;
+  using S = DftShape<P>;
+  constexpr int NG = D::NG, NZ = D::NZ, NGNZ = NG * NZ, PER = FwdCfg<P>::PER, PP = P * P, YO = 2 * PP * NZ;
+  dft_pass<S::KZ, S::NZT>(  // z: lines (t; x, y), real input from UE
+      PP * NBC, NZ, wz,
+      [&](int L, int k) {
+        const int t = L / PP, xy = L - t * PP;
+        if (k >= P) return 0.0;
+        const int m = __ldg(lmap + xy * P + k);
+        return m >= 0 ? __ldg(pick<NB>(src, t, NBC) + m * kml) : 0.0;
+      },
+      [&](int L, int o, double2 v) {
+        const int t = L / PP, xy = L - t * PP;
+        reinterpret_cast<double2*>(sm + t * PER)[xy * NZ + o] = v;
+      });
+  __syncthreads();
+  dft_pass<S::KF, S::NFT>(  // y: lines (t; x, fz)
+      P * NZ * NBC, NG, wf,
+      [&](int L, int k) {
+        const int t = L / (P * NZ), r = L - t * (P * NZ), x = r / NZ, fz = r - x * NZ, y = k >> 1;
+        return y < P ? sm[t * PER + 2 * ((x * P + y) * NZ + fz) + (k & 1)] : 0.0;
+      },
+      [&](int L, int o, double2 v) {
+        const int t = L / (P * NZ), r = L - t * (P * NZ), x = r / NZ, fz = r - x * NZ;
+        reinterpret_cast<double2*>(sm + t * PER + YO)[(x * NG + o) * NZ + fz] = v;
+      });
+  __syncthreads();
+  dft_pass<S::KF, S::NFT>(  // x: lines (fy, fz; t) -> global, frequency major
+      NGNZ * NBC, NG, wf,
+      [&](int L, int k) {
+        const int r = L / NBC, t = L - r * NBC, x = k >> 1;
+        return x < P ? sm[t * PER + YO + 2 * (x * NGNZ + r) + (k & 1)] : 0.0;
+      },
+      [&](int L, int o, double2 v) {
+        const int r = L / NBC, t = L - r * NBC;
+        ub[((int64_t)(o * NGNZ + r) * nq + q) * R + pick<NB>(slot, t, NBC)] = v;
+      });
+}
+
+template <int P, int NB, int NBC>
+__device__ __forceinline__ void fwd_dispatch(int nb, double* sm, const double* (&src)[NB], const int (&slot)[NB],
+                                             const int16_t* lmap, int kml, double2* ub, int64_t nq, int64_t q, int R,
+                                             const double* wz, const double* wf) {
+  if (nb == NBC) fwd_body<P, NB, NBC>(sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf);
+  else if constexpr (NBC > 1) fwd_dispatch<P, NB, NBC - 1>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf);
+}
 
 template <int P, int NB>
 __global__ void __launch_bounds__(256)
     k_fft_fwd(const int32_t* __restrict__ qbox, const int32_t* __restrict__ child, int64_t nq,
-              const double* __restrict__ ue, int ldn, int kml, const int16_t* __restrict__ lat, int M,
+              const double* __restrict__ ue, int ldn, int kml, const int16_t* __restrict__ lmap,
               double2* __restrict__ ub, int zero_missing, const double* __restrict__ wz,
               const double* __restrict__ wf) {
   using D = FftDims<P>;
-  using S = DftShape<P>;
-  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ, PER = FwdCfg<P>::PER;
+  constexpr int NF = D::NF;
   extern __shared__ __align__(16) double sm[];
   const int R = 8 * kml;
   const int ng = (R + NB - 1) / NB;
   const int64_t q = blockIdx.x / ng;
   const int s0 = (blockIdx.x % ng) * NB;
-  const int tid = threadIdx.x, bd = blockDim.x;
   const int64_t qb = qbox[q];
-  // this CTA's transforms: slots with an existing child (missing ones zero-filled / skipped)
+  // this CTA's transforms, compacted: slots with an existing child
+  const double* src[NB];
   int slot[NB];
-  int64_t bx[NB];
   int nb = 0;
-  for (int j = 0; j < NB && s0 + j < R; ++j) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    src[j] = ue;
+    slot[j] = 0;
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
     const int sl = s0 + j;
+    if (sl >= R) break;
     const int64_t b = child[8 * qb + sl / kml];
     if (b >= 0) {
-      slot[nb] = sl;
-      bx[nb] = b;
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (i == nb) {
+          src[i] = ue + b * ldn + sl % kml;
+          slot[i] = sl;
+        }
       ++nb;
     } else if (zero_missing) {
-      for (int f = tid; f < NF; f += bd) ub[((int64_t)f * nq + q) * R + sl] = make_double2(0.0, 0.0);
+      for (int f = threadIdx.x; f < NF; f += blockDim.x) ub[((int64_t)f * nq + q) * R + sl] = make_double2(0.0, 0.0);
     }
   }
   if (nb == 0) return;
-  double* wzs = sm + NB * PER;
-  double* wfs = wzs + D::TZ;
-  stage_table(wzs, wz, D::TZ);
-  stage_table(wfs, wf, D::TF);
-  for (int i = tid; i < nb * D::CUBE; i += bd) sm[(i / D::CUBE) * PER + i % D::CUBE] = 0.0;
-  __syncthreads();
-  for (int i = tid; i < nb * M; i += bd) {
-    const int t = i / M, m = i - t * M;
-    int sl = slot[0];
-    int64_t b = bx[0];
-#pragma unroll
-    for (int j = 1; j < NB; ++j)
-      if (t == j) {
-        sl = slot[j];
-        b = bx[j];
-      }
-    sm[t * PER + (lat[3 * m] * P + lat[3 * m + 1]) * P + lat[3 * m + 2]] = ue[b * ldn + m * kml + sl % kml];
-  }
-  __syncthreads();
-  dft_pass<S::KZ, S::NZT>(  // z: lines (x, y; t), real input
-      P * P * nb, NZ, wzs,
-      [&](int L, int k) {
-        const int xy = L / nb, t = L - xy * nb;
-        return k < P ? sm[t * PER + xy * P + k] : 0.0;
-      },
-      [&](int L, int o, double2 v) {
-        const int xy = L / nb, t = L - xy * nb;
-        reinterpret_cast<double2*>(sm + t * PER + D::CUBE)[xy * NZ + o] = v;
-      });
-  __syncthreads();
-  dft_pass<S::KF, S::NFT>(  // y: lines (x, fz; t)
-      P * NZ * nb, NG, wfs,
-      [&](int L, int k) {
-        const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ, y = k >> 1;
-        const double* A = sm + t * PER + D::CUBE;
-        return y < P ? A[2 * ((x * P + y) * NZ + fz) + (k & 1)] : 0.0;
-      },
-      [&](int L, int o, double2 v) {
-        const int r = L / nb, t = L - r * nb, x = r / NZ, fz = r - x * NZ;
-        reinterpret_cast<double2*>(sm + t * PER + D::CUBE + 2 * P * P * NZ)[(x * NG + o) * NZ + fz] = v;
-      });
-  __syncthreads();
-  dft_pass<S::KF, S::NFT>(  // x: lines (fy, fz; t) -> global, frequency major
-      NGNZ * nb, NG, wfs,
-      [&](int L, int k) {
-        const int r = L / nb, t = L - r * nb, x = k >> 1;
-        const double* B = sm + t * PER + D::CUBE + 2 * P * P * NZ;
-        return x < P ? B[2 * (x * NGNZ + r) + (k & 1)] : 0.0;
-      },
-      [&](int L, int o, double2 v) {
-        const int r = L / nb, t = L - r * nb;
-        int sl = slot[0];
-#pragma unroll
-        for (int j = 1; j < NB; ++j)
-          if (t == j) sl = slot[j];
-        ub[((int64_t)(o * NGNZ + r) * nq + q) * R + sl] = v;
-      });
+  fwd_dispatch<P, NB, NB>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf);
 }
 
-// inverse: one CTA per target box; its check spectrum cb[parent][b kml + a][f] (one contiguous row)
-// -> x and y passes on the tensor cores (outputs only for x, y < p), the z
-// pass evaluated only at the downward-check surface points, times 2^l / NG^3,
-// added to CHK.  NG is odd, so there is no Nyquist bin.
+// inverse: one CTA per target box; its check spectrum cb[parent][b kml + a][f] (one contiguous row,
+// read by the x pass straight from global memory) -> x and y passes on the tensor cores (outputs
+// only for x, y < p), the z pass evaluated only at the downward-check surface points, times
+// 2^l / NG^3, added to CHK.  NG is odd, so there is no Nyquist bin.
 template <int P>
 __global__ void __launch_bounds__(256)
     k_fft_inv(const int32_t* __restrict__ tbox, const int2* __restrict__ tpb, int64_t npar,
@@ -285,13 +292,9 @@ __global__ void __launch_bounds__(256)
   using S = DftShape<P>;
   constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ;
   extern __shared__ __align__(16) double sm[];
-  double2* Sp = reinterpret_cast<double2*>(sm);  // [fx][fy][fz], then E [x][y][fz]
-  double2* Dx = Sp + NF;                          // [x][fy][fz]
-  double2* tw = Dx + P * NG * NZ;                 // exp(+2 pi i j / NG)
-  double2* E = Sp;
-  double* wis = reinterpret_cast<double*>(tw + NG);
-  stage_table(wis, wi, D::TI);
-  const double* Sd = reinterpret_cast<const double*>(Sp);
+  double2* Dx = reinterpret_cast<double2*>(sm);  // [x][fy][fz]
+  double2* E = Dx + P * NG * NZ;                 // [x][y][fz]
+  double2* tw = E + P * P * NZ;                  // exp(+2 pi i j / NG)
   const double* Dd = reinterpret_cast<const double*>(Dx);
   const int t = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
   const int64_t box = tbox[t];
@@ -303,20 +306,20 @@ __global__ void __launch_bounds__(256)
     sincospi(2.0 * j / NG, &sn, &cs);
     tw[j] = make_double2(cs, sn);
   }
+  __syncthreads();
   for (int a = 0; a < kml; ++a) {
-    const double2* col = cb + ((int64_t)pb.x * R + pb.y * kml + a) * NF;  // target-major: one contiguous row
-    for (int f = tid; f < NF; f += bd) Sp[f] = col[f];
-    __syncthreads();
+    // target-major: one contiguous row
+    const double* col = reinterpret_cast<const double*>(cb + ((int64_t)pb.x * R + pb.y * kml + a) * NF);
     dft_pass<S::KI, S::NIT>(  // x: lines (fy, fz), outputs x < P
-        NGNZ, P, wis,
+        NGNZ, P, wi,
         [&](int line, int k) {
           const int fx = k >> 1;
-          return fx < NG ? Sd[2 * (fx * NGNZ + line) + (k & 1)] : 0.0;
+          return fx < NG ? __ldg(col + 2 * (fx * NGNZ + line) + (k & 1)) : 0.0;
         },
         [&](int line, int o, double2 v) { Dx[o * NGNZ + line] = v; });
     __syncthreads();
     dft_pass<S::KI, S::NIT>(  // y: lines (x, fz), outputs y < P
-        P * NZ, P, wis,
+        P * NZ, P, wi,
         [&](int line, int k) {
           const int x = line / NZ, fz = line - x * NZ, fy = k >> 1;
           return fy < NG ? Dd[2 * ((x * NG + fy) * NZ + fz) + (k & 1)] : 0.0;
@@ -524,12 +527,13 @@ static bool chunk_uses_pairs(const Plan& Pl, const FftChunk& ch) {
   return Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < pair_fill_threshold());
 }
 
-// transforms per forward CTA: 4 at p <= 10 (measured: C5 -3%, others equal), 1 above;
-// KAFMM_FWD_NB=1|2|4 overrides (tuning knob; profiles/)
+// transforms per forward CTA: 2 at p <= 10 (measured after the z pass started reading UE
+// directly: C2 M2L transforms 3.5 -> 2.8 ms, nb 1 / 4 slower, profiles/r01_fft_rework_ab.txt),
+// 1 above; KAFMM_FWD_NB=1|2|4 overrides (tuning knob)
 static int fwd_nb(int p) {
   static const char* e = getenv("KAFMM_FWD_NB");
   if (e) return atoi(e) >= 4 ? 4 : (atoi(e) >= 2 ? 2 : 1);
-  return p <= 10 ? 4 : 1;
+  return p <= 10 ? 2 : 1;
 }
 
 template <int P>
@@ -553,7 +557,7 @@ template <int P, int NB>
 static void launch_fwd_nb(Plan& Pl, const FftChunk& ch) {
   const int ng = (8 * Pl.kml + NB - 1) / NB;
   k_fft_fwd<P, NB><<<(unsigned)(ch.nq * ng), 256, FwdCfg<P>::template smem<NB>(), Pl.stream>>>(
-      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lat, Pl.M, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1,
+      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lmap, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1,
       Pl.d_wz, Pl.d_wf);
 }
 
@@ -753,6 +757,13 @@ void build_fft_m2l(Plan& P, int64_t budget) {
         }
   P.d_lat = dalloc<int16_t>(P, lat.size());
   KF_CUDA(cudaMemcpyAsync(P.d_lat, lat.data(), lat.size() * 2, cudaMemcpyHostToDevice, st));
+  {  // p^3 lattice -> surface index (or -1), read by the forward z pass
+    std::vector<int16_t> lmap((size_t)p * p * p, -1);
+    for (size_t m = 0; m < lat.size() / 3; ++m) lmap[((size_t)lat[3 * m] * p + lat[3 * m + 1]) * p + lat[3 * m + 2]] = (int16_t)m;
+    P.d_lmap = dalloc<int16_t>(P, lmap.size());
+    KF_CUDA(cudaMemcpyAsync(P.d_lmap, lmap.data(), lmap.size() * 2, cudaMemcpyHostToDevice, st));
+    KF_CUDA(cudaStreamSynchronize(st));
+  }
   // operator spectra at level 0
   {
     const int NG = P.NG, NG3 = NG * NG * NG, nc = P.ncomp;

@@ -189,6 +189,7 @@ struct Plan {
   int ncomp = 0;                   // stored components per operator spectrum: 1 (L) or 6 (sym. G)
   double2* d_that = nullptr;       // [NF][316][ncomp] operator spectra at level 0
   int16_t* d_lat = nullptr;        // M x 3 integer lattice coordinates of the surface points
+  int16_t* d_lmap = nullptr;       // p^3 lattice -> surface index or -1 (FFT forward z pass)
   int16_t* d_aidx = nullptr;       // DMMA A-fragment gather table [26][8kml/4][kml][32]
   double *d_wz = nullptr, *d_wf = nullptr, *d_wi = nullptr;  // DFT-pass twiddle fragments
   std::vector<FftChunk> fft_chunks;
