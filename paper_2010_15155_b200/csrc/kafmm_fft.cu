@@ -126,33 +126,61 @@ struct DftShape {
 // each DMMA (coalesced, L1-resident: every CTA of the launch reads the same
 // few KB), which keeps the register count low and costs no shared memory
 
+#ifndef KF_DFT_MT
+#define KF_DFT_MT 2
+#endif
+// MT m-tiles of 8 lines at once (independent DMMA accumulator chains: the
+// passes are short, NKS <= 12, so one tile's chains alone leave the tensor
+// pipe waiting on DMMA latency)
+template <int MT, int NKS, int NNT, class LoadA, class StoreC>
+__device__ __forceinline__ void dft_tiles(int mt0, int mstep, int nlines, int nout, const double* __restrict__ wtab,
+                                          LoadA& loadA, StoreC& storeC) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  int line[MT];
+  bool ok[MT];
+  double acc[MT][NNT][2];
+#pragma unroll
+  for (int u = 0; u < MT; ++u) {
+    line[u] = (mt0 + u * mstep) * 8 + g;
+    ok[u] = line[u] < nlines;
+#pragma unroll
+    for (int n = 0; n < NNT; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < NKS; ++k) {
+    double a[MT];
+#pragma unroll
+    for (int u = 0; u < MT; ++u) a[u] = ok[u] ? loadA(line[u], 4 * k + tq) : 0.0;
+#pragma unroll
+    for (int n = 0; n < NNT; ++n) {
+      const double w = __ldg(wtab + (k * NNT + n) * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < MT; ++u) dmma(acc[u][n][0], acc[u][n][1], a[u], w);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < MT; ++u)
+    if (ok[u]) {
+#pragma unroll
+      for (int n = 0; n < NNT; ++n) {
+        const int o = 4 * n + tq;
+        if (o < nout) storeC(line[u], o, make_double2(acc[u][n][0], acc[u][n][1]));
+      }
+    }
+}
+
 // one pass over nlines lines by the CTA's warps; loadA(line, k) -> double,
 // storeC(line, o, double2) for o < nout
 template <int NKS, int NNT, class LoadA, class StoreC>
 __device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __restrict__ wtab, LoadA loadA,
                                          StoreC storeC) {
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, tq = lane & 3;
-  for (int mt = warp; mt * 8 < nlines; mt += nw) {
-    const int line = mt * 8 + g;
-    const bool ok = line < nlines;
-    double acc[NNT][2];
-#pragma unroll
-    for (int n = 0; n < NNT; ++n) acc[n][0] = acc[n][1] = 0.0;
-#pragma unroll
-    for (int k = 0; k < NKS; ++k) {
-      const double a = ok ? loadA(line, 4 * k + tq) : 0.0;
-#pragma unroll
-      for (int n = 0; n < NNT; ++n) dmma(acc[n][0], acc[n][1], a, __ldg(wtab + (k * NNT + n) * 32 + lane));
-    }
-    if (ok) {
-#pragma unroll
-      for (int n = 0; n < NNT; ++n) {
-        const int o = 4 * n + tq;
-        if (o < nout) storeC(line, o, make_double2(acc[n][0], acc[n][1]));
-      }
-    }
-  }
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ntile = (nlines + 7) / 8;
+  int mt = warp;
+#if KF_DFT_MT > 1
+  for (; mt + nw < ntile; mt += 2 * nw) dft_tiles<2, NKS, NNT>(mt, nw, nlines, nout, wtab, loadA, storeC);
+#endif
+  for (; mt < ntile; mt += nw) dft_tiles<1, NKS, NNT>(mt, nw, nlines, nout, wtab, loadA, storeC);
 }
 
 // forward: one CTA per (source parent block q, group of NB transform slots);
