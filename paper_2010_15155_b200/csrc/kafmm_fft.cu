@@ -178,7 +178,8 @@ __device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __r
   const int ntile = (nlines + 7) / 8;
   int mt = warp;
 #if KF_DFT_MT > 1
-  for (; mt + nw < ntile; mt += 2 * nw) dft_tiles<2, NKS, NNT>(mt, nw, nlines, nout, wtab, loadA, storeC);
+  for (; mt + (KF_DFT_MT - 1) * nw < ntile; mt += KF_DFT_MT * nw)
+    dft_tiles<KF_DFT_MT, NKS, NNT>(mt, nw, nlines, nout, wtab, loadA, storeC);
 #endif
   for (; mt < ntile; mt += nw) dft_tiles<1, NKS, NNT>(mt, nw, nlines, nout, wtab, loadA, storeC);
 }
