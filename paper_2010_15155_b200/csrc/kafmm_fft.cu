@@ -509,13 +509,12 @@ __global__ void __launch_bounds__(PAIR_THREADS)
   for (int a = 0; a < KML; ++a) acc[a] = make_double2(0.0, 0.0);
   // pairs in batches of PB: their source spectra are loaded together (memory
   // level parallelism), then the products run from registers
-  constexpr int PB = 4;
+  constexpr int PB = 4;  // lists are padded with -1 to multiples of 4
   const int64_t e1 = off[t + 1];
   for (int64_t e = off[t]; e < e1; e += PB) {
-    int v[PB];
+    const int4 v4 = *reinterpret_cast<const int4*>(pl + e);
+    const int v[PB] = {v4.x, v4.y, v4.z, v4.w};
     double2 u[PB][KML];
-#pragma unroll
-    for (int j = 0; j < PB; ++j) v[j] = e + j < e1 ? pl[e + j] : -1;
 #pragma unroll
     for (int j = 0; j < PB; ++j) {
       const double2* up = ubf + (int64_t)(v[j] >> 9) * KML;
@@ -940,11 +939,12 @@ void build_fft_chunks(Plan& P, int64_t budget) {
           const int oid = offid[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)];
           if (q < 0 || oid < 0) throw Error{KAFMM_ECUDA, "FFT M2L: V source outside the chunk's parent blocks"};
           pl.push_back((int32_t)((q * 8 + c) << 9 | oid));
+          ++ch.npairs;
         }
+        while (pl.size() % 4) pl.push_back(-1);  // 16-B aligned batches of 4 (one vector load per batch)
         ploff.push_back((int64_t)pl.size());
       }
       if ((int64_t)qs.size() * 8 >= (1 << 22)) throw Error{KAFMM_EINVAL, "FFT M2L chunk too large for pair indices"};
-      ch.npairs = (int64_t)pl.size();
       {
         int64_t blocks = 0;
         for (int32_t v : nb) blocks += v >= 0;

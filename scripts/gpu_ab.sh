@@ -1,7 +1,3 @@
-# DFT passes: m-tiles per warp iteration 2 (default) vs 3, 4 (variant libraries)
-for c in 2 4; do
-  timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c${c}_mt2.json 2>>gpurun_out/ab.err
-  for v in mt3 mt4; do
-  KAFMM_LIB=$PWD/paper_2010_15155_b200/libkafmm_$v.so timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c${c}_$v.json 2>>gpurun_out/ab.err
-  done
-done
+# sparse-chunk product: 16-B pair-list batches
+timeout 900 python -m pytest tests/test_gpu_m2l_modes.py -x -q > gpurun_out/ab_pytest.log 2>&1; echo pytest=$?; tail -2 gpurun_out/ab_pytest.log
+timeout 600 python bench.py --config 5 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c5.json 2>>gpurun_out/ab.err
