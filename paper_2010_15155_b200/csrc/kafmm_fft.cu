@@ -215,7 +215,7 @@ template <int P, int NB, int NBC>
 __device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* (&src)[NB], const int (&slot)[NB],
                                          const int16_t* __restrict__ lmap, int kml, double2* __restrict__ ub,
                                          int64_t nq, int64_t q, int R, const double* __restrict__ wz,
-                                         const double* __restrict__ wf) {
+                                         const double* __restrict__ wf, bool blocked) {
   using D = FftDims<P>;
   using S = DftShape<P>;
   constexpr int NG = D::NG, NZ = D::NZ, NGNZ = NG * NZ, PER = FwdCfg<P>::PER, PP = P * P, YO = 2 * PP * NZ;
@@ -250,17 +250,21 @@ __device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* 
         return x < P ? sm[t * PER + YO + 2 * (x * NGNZ + r) + (k & 1)] : 0.0;
       },
       [&](int L, int o, double2 v) {
-        const int r = L / NBC, t = L - r * NBC;
-        ub[((int64_t)(o * NGNZ + r) * nq + q) * R + pick<NB>(slot, t, NBC)] = v;
+        const int r = L / NBC, t = L - r * NBC, f = o * NGNZ + r, sl = pick<NB>(slot, t, NBC);
+        if (blocked)  // per-pair chunks: [f / 4][q][R][f % 4] (k_m2l_pairs4)
+          ub[(((int64_t)(f >> 2) * nq + q) * R + sl) * 4 + (f & 3)] = v;
+        else
+          ub[((int64_t)f * nq + q) * R + sl] = v;
       });
 }
 
 template <int P, int NB, int NBC>
 __device__ __forceinline__ void fwd_dispatch(int nb, double* sm, const double* (&src)[NB], const int (&slot)[NB],
                                              const int16_t* lmap, int kml, double2* ub, int64_t nq, int64_t q, int R,
-                                             const double* wz, const double* wf) {
-  if (nb == NBC) fwd_body<P, NB, NBC>(sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf);
-  else if constexpr (NBC > 1) fwd_dispatch<P, NB, NBC - 1>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf);
+                                             const double* wz, const double* wf, bool blocked) {
+  if (nb == NBC) fwd_body<P, NB, NBC>(sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf, blocked);
+  else if constexpr (NBC > 1)
+    fwd_dispatch<P, NB, NBC - 1>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf, blocked);
 }
 
 template <int P, int NB>
@@ -304,7 +308,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   if (nb == 0) return;
-  fwd_dispatch<P, NB, NB>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf);
+  fwd_dispatch<P, NB, NB>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf, !zero_missing);
 }
 
 // inverse: one CTA per target box; its check spectrum cb[parent][b kml + a][f] (one contiguous row,
@@ -481,71 +485,80 @@ __global__ void __launch_bounds__(DM_WARPS * 32, KML == 1 ? KF_DMMA_MINB1 : KF_D
 }
 
 // The same product per V pair, for chunks whose parent blocks are mostly
-// empty (sparse adaptive trees): one thread per (target box, frequency), the
-// frequency's operator spectra in shared memory, the target's V list walked
-// with the source spectra read from ub and the sum kept in registers.
-constexpr int PAIR_THREADS = 128;
+// empty (sparse adaptive trees).
+// The per-pair product with 4 frequencies per target: a warp is 8 targets x 4
+// consecutive frequencies (lane = 4 t + fi), so the 4 lanes of a target read
+// one 64-B run of operator spectra (SMEM, [c][offset][4 f]) and one 64-B run
+// of source spectra (ub in the blocked layout [f / 4][q][8 kml][f % 4] that
+// the forward transform writes for these chunks) per pair and component,
+// instead of 16-B gathers at random banks / lines.  A CTA stages the 4
+// frequencies' operator spectra once and walks P4_TB target blocks.
+constexpr int P4_THREADS = 512, P4_TPB = P4_THREADS / 4, P4_TB = 8;
 
 template <int KML>
-__global__ void __launch_bounds__(PAIR_THREADS)
-    k_m2l_pairs(int64_t nt, int64_t nq, int64_t npar, int ntb, const double2* __restrict__ that,
-                const double2* __restrict__ ub, double2* __restrict__ cb, const int2* __restrict__ tpb,
-                const int64_t* __restrict__ off, const int32_t* __restrict__ pl) {
+__global__ void __launch_bounds__(P4_THREADS)
+    k_m2l_pairs4(int64_t nt, int64_t nq, int ntb, int NF, const double2* __restrict__ that,
+                 const double2* __restrict__ ub, double2* __restrict__ cb, const int2* __restrict__ tpb,
+                 const int64_t* __restrict__ off, const int32_t* __restrict__ pl) {
   constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
-  const int64_t NF = gridDim.x / ntb;  // grid = target blocks x frequency bins
-  // operator spectra of this frequency as NC planes of 316 complex: lanes that
-  // gather different offsets spread over 8 bank groups (a 96-B record stride
-  // would hit only 4)
-  __shared__ double2 sT[NC][N_OFFSETS];
-  const int64_t f = blockIdx.x / ntb;
-  const int tb = blockIdx.x % ntb;
-  for (int i = threadIdx.x; i < N_OFFSETS * NC; i += PAIR_THREADS) sT[i % NC][i / NC] = that[f * N_OFFSETS * NC + i];
+  extern __shared__ double2 sT4[];  // [NC][N_OFFSETS][4]
+  const int ngrp = (ntb + P4_TB - 1) / P4_TB;
+  const int fb = blockIdx.x / ngrp, grp = blockIdx.x % ngrp;
+  for (int i = threadIdx.x; i < N_OFFSETS * NC * 4; i += P4_THREADS) {
+    const int fi = i & 3, oc = i >> 2, c = oc / N_OFFSETS, o = oc - c * N_OFFSETS;
+    const int f = fb * 4 + fi;
+    sT4[i] = f < NF ? that[((int64_t)f * N_OFFSETS + o) * NC + c] : make_double2(0.0, 0.0);
+  }
   __syncthreads();
-  const int64_t t = (int64_t)tb * PAIR_THREADS + threadIdx.x;
-  if (t >= nt) return;
-  const double2* ubf = ub + f * nq * R;
-  double2 acc[KML];
+  const int fi = threadIdx.x & 3, f = fb * 4 + fi;
+  const double2* ubb = ub + (int64_t)fb * nq * R * 4 + fi;
+  const double2* sTf = sT4 + fi;
+  for (int tb = grp * P4_TB; tb < min(ntb, (grp + 1) * P4_TB); ++tb) {
+    const int64_t t = (int64_t)tb * P4_TPB + (threadIdx.x >> 2);
+    if (t >= nt) break;
+    double2 acc[KML];
 #pragma unroll
-  for (int a = 0; a < KML; ++a) acc[a] = make_double2(0.0, 0.0);
-  // pairs in batches of PB: their source spectra are loaded together (memory
-  // level parallelism), then the products run from registers
-  constexpr int PB = 4;  // lists are padded with -1 to multiples of 4
-  const int64_t e1 = off[t + 1];
-  for (int64_t e = off[t]; e < e1; e += PB) {
-    const int4 v4 = *reinterpret_cast<const int4*>(pl + e);
-    const int v[PB] = {v4.x, v4.y, v4.z, v4.w};
-    double2 u[PB][KML];
+    for (int a = 0; a < KML; ++a) acc[a] = make_double2(0.0, 0.0);
+    const int64_t e1 = off[t + 1];
+    for (int64_t e = off[t]; e < e1; e += 4) {  // lists padded with -1 to multiples of 4
+      const int4 v4 = *reinterpret_cast<const int4*>(pl + e);
+      const int v[4] = {v4.x, v4.y, v4.z, v4.w};
+      double2 u[4][KML];
 #pragma unroll
-    for (int j = 0; j < PB; ++j) {
-      const double2* up = ubf + (int64_t)(v[j] >> 9) * KML;
+      for (int j = 0; j < 4; ++j) {
+        const double2* up = ubb + (int64_t)(v[j] >> 9) * KML * 4;
 #pragma unroll
-      for (int a = 0; a < KML; ++a) u[j][a] = v[j] >= 0 ? up[a] : make_double2(0.0, 0.0);
-    }
+        for (int a = 0; a < KML; ++a) u[j][a] = v[j] >= 0 ? up[a * 4] : make_double2(0.0, 0.0);
+      }
 #pragma unroll
-    for (int j = 0; j < PB; ++j) {
-      const int o = v[j] >= 0 ? (v[j] & 511) : 0;
-      if (KML == 1) {
-        cmac(acc[0], sT[0][o], u[j][0]);
-      } else {
-        const double2 t0 = sT[0][o], t1 = sT[NC > 1 ? 1 : 0][o], t2 = sT[NC > 2 ? 2 : 0][o],
-                      t3 = sT[NC > 3 ? 3 : 0][o], t4 = sT[NC > 4 ? 4 : 0][o], t5 = sT[NC > 5 ? 5 : 0][o];
-        const double2 u0 = u[j][0], u1 = u[j][KML > 1 ? 1 : 0], u2 = u[j][KML > 2 ? 2 : 0];
-        cmac(acc[0], t0, u0);
-        cmac(acc[0], t1, u1);
-        cmac(acc[0], t2, u2);
-        cmac(acc[KML > 1 ? 1 : 0], t1, u0);
-        cmac(acc[KML > 1 ? 1 : 0], t3, u1);
-        cmac(acc[KML > 1 ? 1 : 0], t4, u2);
-        cmac(acc[KML > 2 ? 2 : 0], t2, u0);
-        cmac(acc[KML > 2 ? 2 : 0], t4, u1);
-        cmac(acc[KML > 2 ? 2 : 0], t5, u2);
+      for (int j = 0; j < 4; ++j) {
+        const int o4 = (v[j] >= 0 ? (v[j] & 511) : 0) * 4;
+        if (KML == 1) {
+          cmac(acc[0], sTf[o4], u[j][0]);
+        } else {
+          constexpr int CS = N_OFFSETS * 4;
+          const double2 t0 = sTf[o4], t1 = sTf[CS + o4], t2 = sTf[2 * CS + o4], t3 = sTf[(NC > 3 ? 3 : 0) * CS + o4],
+                        t4 = sTf[(NC > 4 ? 4 : 0) * CS + o4], t5 = sTf[(NC > 5 ? 5 : 0) * CS + o4];
+          const double2 u0 = u[j][0], u1 = u[j][KML > 1 ? 1 : 0], u2 = u[j][KML > 2 ? 2 : 0];
+          cmac(acc[0], t0, u0);
+          cmac(acc[0], t1, u1);
+          cmac(acc[0], t2, u2);
+          cmac(acc[KML > 1 ? 1 : 0], t1, u0);
+          cmac(acc[KML > 1 ? 1 : 0], t3, u1);
+          cmac(acc[KML > 1 ? 1 : 0], t4, u2);
+          cmac(acc[KML > 2 ? 2 : 0], t2, u0);
+          cmac(acc[KML > 2 ? 2 : 0], t4, u1);
+          cmac(acc[KML > 2 ? 2 : 0], t5, u2);
+        }
       }
     }
-  }
-  const int2 pb = tpb[t];
-  double2* o = cb + ((int64_t)pb.x * R + pb.y * KML) * NF + f;
+    if (f < NF) {
+      const int2 pb = tpb[t];
+      double2* o = cb + ((int64_t)pb.x * R + pb.y * KML) * NF + f;
 #pragma unroll
-  for (int a = 0; a < KML; ++a) o[(int64_t)a * NF] = acc[a];
+      for (int a = 0; a < KML; ++a) o[(int64_t)a * NF] = acc[a];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -637,16 +650,26 @@ void run_m2l_fft(Plan& Pl) {
     const bool pairs = chunk_uses_pairs(Pl, ch);
     prod_mark(Pl);
     if (pairs) {
-      const int ntb = (int)((ch.nt + PAIR_THREADS - 1) / PAIR_THREADS);
-      const unsigned grid = (unsigned)((int64_t)ntb * Pl.NF);
-      // (a tensor-core variant that grouped a tile's pairs by offset measured 3.3x slower
-      // on C5, staging bound: profiles/r01_C5_pairs_ab.txt; removed after round 1)
+      // 4 frequencies per target (blocked ub layout; a thread per (target, frequency) with
+      // 16-B gathers measured 1163 ms on C5, profiles/r01_pairs4_ab.txt)
+      const int ntb = (int)((ch.nt + P4_TPB - 1) / P4_TPB);
+      const int ngrp = (ntb + P4_TB - 1) / P4_TB, nfb = (int)((Pl.NF + 3) / 4);
+      const unsigned grid = (unsigned)((int64_t)ngrp * nfb);
+      const size_t smem = (size_t)N_OFFSETS * (Pl.kml == 1 ? 1 : 6) * 4 * sizeof(double2);
+      static bool attr = false;
+      if (!attr) {
+        KF_CUDA(cudaFuncSetAttribute(k_m2l_pairs4<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(N_OFFSETS * 4 * sizeof(double2))));
+        KF_CUDA(cudaFuncSetAttribute(k_m2l_pairs4<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(N_OFFSETS * 6 * 4 * sizeof(double2))));
+        attr = true;
+      }
       if (Pl.kml == 1)
-        k_m2l_pairs<1><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
-                                                             Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
+        k_m2l_pairs4<1><<<grid, P4_THREADS, smem, Pl.stream>>>(ch.nt, ch.nq, ntb, (int)Pl.NF, Pl.d_that, Pl.d_ub,
+                                                               Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
       else
-        k_m2l_pairs<3><<<grid, PAIR_THREADS, 0, Pl.stream>>>(ch.nt, ch.nq, ch.npar, ntb, Pl.d_that, Pl.d_ub,
-                                                             Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
+        k_m2l_pairs4<3><<<grid, P4_THREADS, smem, Pl.stream>>>(ch.nt, ch.nq, ntb, (int)Pl.NF, Pl.d_that, Pl.d_ub,
+                                                               Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
     } else {
       // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
       // (fewer registers, more resident warps) -- a tuning knob measured in profiles/
@@ -979,7 +1002,7 @@ void build_fft_chunks(Plan& P, int64_t budget) {
   }
   dfree(P, P.d_ub);
   dfree(P, P.d_cb);
-  P.d_ub = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_nq) * R * P.NF);
+  P.d_ub = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_nq) * R * ((P.NF + 3) / 4 * 4));
   P.d_cb = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_npar) * R * P.NF);
 }
 
