@@ -493,7 +493,10 @@ __global__ void __launch_bounds__(DM_WARPS * 32, KML == 1 ? KF_DMMA_MINB1 : KF_D
 // the forward transform writes for these chunks) per pair and component,
 // instead of 16-B gathers at random banks / lines.  A CTA stages the 4
 // frequencies' operator spectra once and walks P4_TB target blocks.
-constexpr int P4_THREADS = 512, P4_TPB = P4_THREADS / 4, P4_TB = 8;
+#ifndef KF_P4_THREADS
+#define KF_P4_THREADS 1024  // 32 warps per SM (registers allow no more): C5 product 671 -> 610 ms vs 512
+#endif
+constexpr int P4_THREADS = KF_P4_THREADS, P4_TPB = P4_THREADS / 4, P4_TB = 8;
 
 template <int KML>
 __global__ void __launch_bounds__(P4_THREADS)
