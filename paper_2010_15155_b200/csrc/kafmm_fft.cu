@@ -86,6 +86,13 @@ __global__ void k_spectra_transpose(int NF, int nc, const double2* __restrict__ 
 // ---------------------------------------------------------------------------
 // hot path kernels
 // ---------------------------------------------------------------------------
+// frequencies per target lane group of the per-pair product (k_m2l_pairsf), which is
+// also the frequency block of ub in per-pair chunks
+#ifndef KF_PAIR_FB
+#define KF_PAIR_FB 8
+#endif
+constexpr int PFB = KF_PAIR_FB;
+
 template <int P>
 struct FftDims {
   static constexpr int NG = 2 * P - 1, NZ = NG / 2 + 1, NF = NG * NG * NZ;
@@ -251,8 +258,8 @@ __device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* 
       },
       [&](int L, int o, double2 v) {
         const int r = L / NBC, t = L - r * NBC, f = o * NGNZ + r, sl = pick<NB>(slot, t, NBC);
-        if (blocked)  // per-pair chunks: [f / 4][q][R][f % 4] (k_m2l_pairs4)
-          ub[(((int64_t)(f >> 2) * nq + q) * R + sl) * 4 + (f & 3)] = v;
+        if (blocked)  // per-pair chunks: [f / PFB][q][R][f % PFB] (k_m2l_pairsf)
+          ub[(((int64_t)(f / PFB) * nq + q) * R + sl) * PFB + (f % PFB)] = v;
         else
           ub[((int64_t)f * nq + q) * R + sl] = v;
       });
@@ -486,38 +493,43 @@ __global__ void __launch_bounds__(DM_WARPS * 32, KML == 1 ? KF_DMMA_MINB1 : KF_D
 
 // The same product per V pair, for chunks whose parent blocks are mostly
 // empty (sparse adaptive trees).
-// The per-pair product with 4 frequencies per target: a warp is 8 targets x 4
-// consecutive frequencies (lane = 4 t + fi), so the 4 lanes of a target read
-// one 64-B run of operator spectra (SMEM, [c][offset][4 f]) and one 64-B run
-// of source spectra (ub in the blocked layout [f / 4][q][8 kml][f % 4] that
-// the forward transform writes for these chunks) per pair and component,
-// instead of 16-B gathers at random banks / lines.  A CTA stages the 4
-// frequencies' operator spectra once and walks P4_TB target blocks.
-#ifndef KF_P4_THREADS
-#define KF_P4_THREADS 1024  // 32 warps per SM (registers allow no more): C5 product 671 -> 610 ms vs 512
+// The per-pair product with PFB consecutive frequencies per target: a warp is
+// 32/PFB targets x PFB frequencies (lane = PFB t + fi), so the lanes of a
+// target read one contiguous 16 PFB-byte run of operator spectra (SMEM) and of
+// source spectra (ub in the blocked layout [f / PFB][q][8 kml][f % PFB] that the
+// forward transform writes for these chunks) per pair and component, instead
+// of 16-B gathers at random banks / lines.  The operator spectra are even in
+// the offset (G(-r) = G(r) and the lattice differences are symmetric), so
+// T_{-o}(f) = conj T_o(f): SMEM holds the 158 offsets o < 158 ([c][o][PFB f]),
+// offset 315 - o is -o (the offset table is ordered lexicographically over a
+// symmetric set) and is read as the conjugate.  A CTA stages its frequencies'
+// spectra once and walks PF_TB target blocks.
+#ifndef KF_PF_THREADS
+#define KF_PF_THREADS 1024  // 32 warps per SM (registers allow no more)
 #endif
-constexpr int P4_THREADS = KF_P4_THREADS, P4_TPB = P4_THREADS / 4, P4_TB = 8;
+constexpr int PF_THREADS = KF_PF_THREADS, PF_TPB = PF_THREADS / PFB, PF_TB = 8;
+constexpr int N_HALF = N_OFFSETS / 2;  // 158
 
 template <int KML>
-__global__ void __launch_bounds__(P4_THREADS)
-    k_m2l_pairs4(int64_t nt, int64_t nq, int ntb, int NF, const double2* __restrict__ that,
+__global__ void __launch_bounds__(PF_THREADS)
+    k_m2l_pairsf(int64_t nt, int64_t nq, int ntb, int NF, const double2* __restrict__ that,
                  const double2* __restrict__ ub, double2* __restrict__ cb, const int2* __restrict__ tpb,
                  const int64_t* __restrict__ off, const int32_t* __restrict__ pl) {
-  constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
-  extern __shared__ double2 sT4[];  // [NC][N_OFFSETS][4]
-  const int ngrp = (ntb + P4_TB - 1) / P4_TB;
+  constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML, CS = N_HALF * PFB;
+  extern __shared__ double2 sTh[];  // [NC][N_HALF][PFB]
+  const int ngrp = (ntb + PF_TB - 1) / PF_TB;
   const int fb = blockIdx.x / ngrp, grp = blockIdx.x % ngrp;
-  for (int i = threadIdx.x; i < N_OFFSETS * NC * 4; i += P4_THREADS) {
-    const int fi = i & 3, oc = i >> 2, c = oc / N_OFFSETS, o = oc - c * N_OFFSETS;
-    const int f = fb * 4 + fi;
-    sT4[i] = f < NF ? that[((int64_t)f * N_OFFSETS + o) * NC + c] : make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < N_HALF * NC * PFB; i += PF_THREADS) {
+    const int fi = i % PFB, oc = i / PFB, c = oc / N_HALF, o = oc - c * N_HALF;
+    const int f = fb * PFB + fi;
+    sTh[i] = f < NF ? that[((int64_t)f * N_OFFSETS + o) * NC + c] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const int fi = threadIdx.x & 3, f = fb * 4 + fi;
-  const double2* ubb = ub + (int64_t)fb * nq * R * 4 + fi;
-  const double2* sTf = sT4 + fi;
-  for (int tb = grp * P4_TB; tb < min(ntb, (grp + 1) * P4_TB); ++tb) {
-    const int64_t t = (int64_t)tb * P4_TPB + (threadIdx.x >> 2);
+  const int fi = threadIdx.x % PFB, f = fb * PFB + fi;
+  const double2* ubb = ub + (int64_t)fb * nq * R * PFB + fi;
+  const double2* sTf = sTh + fi;
+  for (int tb = grp * PF_TB; tb < min(ntb, (grp + 1) * PF_TB); ++tb) {
+    const int64_t t = (int64_t)tb * PF_TPB + threadIdx.x / PFB;
     if (t >= nt) break;
     double2 acc[KML];
 #pragma unroll
@@ -529,19 +541,25 @@ __global__ void __launch_bounds__(P4_THREADS)
       double2 u[4][KML];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const double2* up = ubb + (int64_t)(v[j] >> 9) * KML * 4;
+        const double2* up = ubb + (int64_t)(v[j] >> 9) * KML * PFB;
 #pragma unroll
-        for (int a = 0; a < KML; ++a) u[j][a] = v[j] >= 0 ? up[a * 4] : make_double2(0.0, 0.0);
+        for (int a = 0; a < KML; ++a) u[j][a] = v[j] >= 0 ? up[a * PFB] : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int o4 = (v[j] >= 0 ? (v[j] & 511) : 0) * 4;
+        const int o = v[j] >= 0 ? (v[j] & 511) : 0;
+        const bool cj = o >= N_HALF;
+        const int oo = (cj ? N_OFFSETS - 1 - o : o) * PFB;
+        const double sg = cj ? -1.0 : 1.0;
+        auto T = [&](int c) {
+          const double2 t = sTf[c * CS + oo];
+          return make_double2(t.x, sg * t.y);
+        };
         if (KML == 1) {
-          cmac(acc[0], sTf[o4], u[j][0]);
+          cmac(acc[0], T(0), u[j][0]);
         } else {
-          constexpr int CS = N_OFFSETS * 4;
-          const double2 t0 = sTf[o4], t1 = sTf[CS + o4], t2 = sTf[2 * CS + o4], t3 = sTf[(NC > 3 ? 3 : 0) * CS + o4],
-                        t4 = sTf[(NC > 4 ? 4 : 0) * CS + o4], t5 = sTf[(NC > 5 ? 5 : 0) * CS + o4];
+          const double2 t0 = T(0), t1 = T(1), t2 = T(2), t3 = T(NC > 3 ? 3 : 0), t4 = T(NC > 4 ? 4 : 0),
+                        t5 = T(NC > 5 ? 5 : 0);
           const double2 u0 = u[j][0], u1 = u[j][KML > 1 ? 1 : 0], u2 = u[j][KML > 2 ? 2 : 0];
           cmac(acc[0], t0, u0);
           cmac(acc[0], t1, u1);
@@ -653,25 +671,25 @@ void run_m2l_fft(Plan& Pl) {
     const bool pairs = chunk_uses_pairs(Pl, ch);
     prod_mark(Pl);
     if (pairs) {
-      // 4 frequencies per target (blocked ub layout; a thread per (target, frequency) with
+      // PFB frequencies per target (blocked ub layout; a thread per (target, frequency) with
       // 16-B gathers measured 1163 ms on C5, profiles/r01_pairs4_ab.txt)
-      const int ntb = (int)((ch.nt + P4_TPB - 1) / P4_TPB);
-      const int ngrp = (ntb + P4_TB - 1) / P4_TB, nfb = (int)((Pl.NF + 3) / 4);
+      const int ntb = (int)((ch.nt + PF_TPB - 1) / PF_TPB);
+      const int ngrp = (ntb + PF_TB - 1) / PF_TB, nfb = (int)((Pl.NF + PFB - 1) / PFB);
       const unsigned grid = (unsigned)((int64_t)ngrp * nfb);
-      const size_t smem = (size_t)N_OFFSETS * (Pl.kml == 1 ? 1 : 6) * 4 * sizeof(double2);
+      const size_t smem = (size_t)N_HALF * (Pl.kml == 1 ? 1 : 6) * PFB * sizeof(double2);
       static bool attr = false;
       if (!attr) {
-        KF_CUDA(cudaFuncSetAttribute(k_m2l_pairs4<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(N_OFFSETS * 4 * sizeof(double2))));
-        KF_CUDA(cudaFuncSetAttribute(k_m2l_pairs4<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(N_OFFSETS * 6 * 4 * sizeof(double2))));
+        KF_CUDA(cudaFuncSetAttribute(k_m2l_pairsf<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(N_HALF * PFB * sizeof(double2))));
+        KF_CUDA(cudaFuncSetAttribute(k_m2l_pairsf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(N_HALF * 6 * PFB * sizeof(double2))));
         attr = true;
       }
       if (Pl.kml == 1)
-        k_m2l_pairs4<1><<<grid, P4_THREADS, smem, Pl.stream>>>(ch.nt, ch.nq, ntb, (int)Pl.NF, Pl.d_that, Pl.d_ub,
+        k_m2l_pairsf<1><<<grid, PF_THREADS, smem, Pl.stream>>>(ch.nt, ch.nq, ntb, (int)Pl.NF, Pl.d_that, Pl.d_ub,
                                                                Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
       else
-        k_m2l_pairs4<3><<<grid, P4_THREADS, smem, Pl.stream>>>(ch.nt, ch.nq, ntb, (int)Pl.NF, Pl.d_that, Pl.d_ub,
+        k_m2l_pairsf<3><<<grid, PF_THREADS, smem, Pl.stream>>>(ch.nt, ch.nq, ntb, (int)Pl.NF, Pl.d_that, Pl.d_ub,
                                                                Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
     } else {
       // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
@@ -1005,7 +1023,7 @@ void build_fft_chunks(Plan& P, int64_t budget) {
   }
   dfree(P, P.d_ub);
   dfree(P, P.d_cb);
-  P.d_ub = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_nq) * R * ((P.NF + 3) / 4 * 4));
+  P.d_ub = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_nq) * R * ((P.NF + PFB - 1) / PFB * PFB));
   P.d_cb = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_npar) * R * P.NF);
 }
 
