@@ -1,6 +1,5 @@
-# per-pair product: 8 frequencies per target + conjugate-symmetric half table (default), 4 frequencies, 512 threads
-timeout 900 python -m pytest tests/test_gpu_m2l_modes.py -x -q > gpurun_out/ab_pytest.log 2>&1; echo pytest=$?; tail -2 gpurun_out/ab_pytest.log
-timeout 600 python bench.py --config 5 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c5_fb8.json 2>>gpurun_out/ab.err
-for v in fb4 fb8t512; do
-KAFMM_LIB=$PWD/paper_2010_15155_b200/libkafmm_$v.so timeout 600 python bench.py --config 5 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c5_$v.json 2>>gpurun_out/ab.err
-done
+timeout 1200 ncu -f --set full --clock-control none --import-source on -k regex:'k_leaf_far' -c 1 -o /tmp/c5_lf python scripts/profile_eval.py 5 1 > gpurun_out/ncu_lf.log 2>&1; echo ncu=$?
+timeout 1200 ncu -f --set full --clock-control none --import-source on -k regex:'k_points_to_surface' -s 1 -c 1 -o /tmp/c5_s2l python scripts/profile_eval.py 5 1 > gpurun_out/ncu_s2l.log 2>&1; echo ncu=$?
+python scripts/ncu_summary.py /tmp/c5_lf.ncu-rep > gpurun_out/c5_lf_summary.txt 2>&1
+python scripts/ncu_summary.py /tmp/c5_s2l.ncu-rep >> gpurun_out/c5_lf_summary.txt 2>&1
+cp /tmp/c5_lf.ncu-rep /tmp/c5_s2l.ncu-rep gpurun_out/
