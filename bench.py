@@ -329,6 +329,8 @@ def main():
         run_e2e(hsrc, hout)
         et = []
         for _ in range(args.steps):
+            flush.fill_(1.0)   # same cold-L2 start as the device-timed steps
+            torch.cuda.synchronize()
             barrier()
             t0 = time.perf_counter()
             run_e2e(hsrc, hout)
@@ -357,7 +359,9 @@ def main():
         m2l_flop = 8.0 * kml * kml * nf * n_v_local
         algo = (f"FFT M2L: 8 kml^2 flop per V pair per frequency bin, kml={kml}, NF={nf} (grid {ng}^3), "
                 f"{n_v_local} V pairs = {m2l_flop:.3e} flop")
-        kname = "m2l product (k_m2l_dmma: per-frequency complex GEMM over parent blocks, DMMA.8x8x4)"
+        kname = ("m2l product: k_m2l_dmma (dense chunks: per-frequency complex GEMM over parent blocks, "
+                 "DMMA.8x8x4, 3 real products per complex multiply-add = 6 of the 8 algorithmic flops) + "
+                 "k_m2l_pairsf (sparse chunks: per V pair on the DFMA pipe)")
     else:
         m2l_flop = 2.0 * n * n * n_v_local
         algo = f"dense M2L: 2 n^2 flop per V pair, n={n}, {n_v_local} pairs = {m2l_flop:.3e} flop"
