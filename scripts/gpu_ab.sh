@@ -1,5 +1,6 @@
-timeout 1200 ncu -f --set full --clock-control none --import-source on -k regex:'k_leaf_far' -c 1 -o /tmp/c5_lf python scripts/profile_eval.py 5 1 > gpurun_out/ncu_lf.log 2>&1; echo ncu=$?
-timeout 1200 ncu -f --set full --clock-control none --import-source on -k regex:'k_points_to_surface' -s 1 -c 1 -o /tmp/c5_s2l python scripts/profile_eval.py 5 1 > gpurun_out/ncu_s2l.log 2>&1; echo ncu=$?
-python scripts/ncu_summary.py /tmp/c5_lf.ncu-rep > gpurun_out/c5_lf_summary.txt 2>&1
-python scripts/ncu_summary.py /tmp/c5_s2l.ncu-rep >> gpurun_out/c5_lf_summary.txt 2>&1
-cp /tmp/c5_lf.ncu-rep /tmp/c5_s2l.ncu-rep gpurun_out/
+# forward DFT: densities + lattice map staged in SMEM (new) vs read through L1 (prev)
+timeout 900 python -m pytest tests/test_gpu_m2l_modes.py tests/test_gpu_edge.py -x -q -k "modes or orders or single" > gpurun_out/ab_pytest.log 2>&1; echo pytest=$?; tail -1 gpurun_out/ab_pytest.log
+for c in 2 3 5; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c${c}_new.json 2>>gpurun_out/ab.err
+  KAFMM_LIB=$PWD/paper_2010_15155_b200/libkafmm_prev.so timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c${c}_prev.json 2>>gpurun_out/ab.err
+done
