@@ -1,5 +1,3 @@
-# final check after the LapPGradGrad functor change: full GPU suite, C2 default line, C9
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/fin2_pytest.log 2>&1; echo pytest=$?; tail -1 gpurun_out/fin2_pytest.log
-timeout 900 python bench.py > gpurun_out/fin2_bench_c2.json 2> gpurun_out/fin2_bench_c2.err; echo bench=$?
-timeout 900 python bench.py --config 9 --steps 3 --no-cpu-baseline > gpurun_out/fin2_bench_c9.json 2>> gpurun_out/fin2_bench_c2.err; echo bench9=$?
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin2_smoke.log 2>&1; echo smoke=$?
+# LapQPGradGrad pair functor in fused form
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_wall.py tests/test_gpu_fullsize.py tests/test_gpu_edge.py -x -q -k "qp or C9 or wall or single or leaves" > gpurun_out/ab_pytest.log 2>&1; echo pytest=$?; tail -1 gpurun_out/ab_pytest.log
+timeout 600 python bench.py --config 9 --no-cpu-baseline --steps 3 > gpurun_out/ab_c9_new.json 2>>gpurun_out/ab.err
