@@ -1,3 +1,3 @@
-# LapQPGradGrad pair functor in fused form
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_wall.py tests/test_gpu_fullsize.py tests/test_gpu_edge.py -x -q -k "qp or C9 or wall or single or leaves" > gpurun_out/ab_pytest.log 2>&1; echo pytest=$?; tail -1 gpurun_out/ab_pytest.log
-timeout 600 python bench.py --config 9 --no-cpu-baseline --steps 3 > gpurun_out/ab_c9_new.json 2>>gpurun_out/ab.err
+# the N-GPU bench path (torchrun + NCCL) at world size 1 on the final code
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --dist --steps 3 --warmup 3 > gpurun_out/dist1.json 2> gpurun_out/dist1.err; echo dist=$?
+( time timeout 900 python bench.py --impl reference --steps 2 --warmup 1 ) > gpurun_out/ref.json 2> gpurun_out/ref.err; echo ref=$?
