@@ -400,7 +400,10 @@ __global__ void __launch_bounds__(256)
 //     Re = P1 - P2,  Im = P3 - P1 - P2,
 // the sums a + b and c + d formed in registers (one DADD per fragment),
 // the three accumulators combined once in the epilogue.
-constexpr int DM_WARPS = 4;
+#ifndef KF_DM_WARPS
+#define KF_DM_WARPS 4
+#endif
+constexpr int DM_WARPS = KF_DM_WARPS;
 
 #ifndef KF_DMMA_MINB1
 #define KF_DMMA_MINB1 1

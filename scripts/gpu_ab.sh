@@ -1,3 +1,9 @@
-# the N-GPU bench path (torchrun + NCCL) at world size 1 on the final code
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --dist --steps 3 --warmup 3 > gpurun_out/dist1.json 2> gpurun_out/dist1.err; echo dist=$?
-( time timeout 900 python bench.py --impl reference --steps 2 --warmup 1 ) > gpurun_out/ref.json 2> gpurun_out/ref.err; echo ref=$?
+# product CTA shape: warps per CTA x parent n-tiles per warp
+timeout 600 python bench.py --config 2 --no-cpu-baseline --no-e2e --steps 5 > gpurun_out/ab_c2_base.json 2>>gpurun_out/ab.err
+for v in w8nt2 w8nt4 w2nt4; do
+  KAFMM_LIB=$PWD/paper_2010_15155_b200/libkafmm_$v.so timeout 600 python bench.py --config 2 --no-cpu-baseline --no-e2e --steps 5 > gpurun_out/ab_c2_$v.json 2>>gpurun_out/ab.err
+done
+timeout 600 python bench.py --config 3 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c3_base.json 2>>gpurun_out/ab.err
+for v in w8nt2 w2nt4; do
+  KAFMM_LIB=$PWD/paper_2010_15155_b200/libkafmm_$v.so timeout 600 python bench.py --config 3 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c3_$v.json 2>>gpurun_out/ab.err
+done
