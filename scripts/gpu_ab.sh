@@ -1,9 +1,6 @@
-# product CTA shape: warps per CTA x parent n-tiles per warp
-timeout 600 python bench.py --config 2 --no-cpu-baseline --no-e2e --steps 5 > gpurun_out/ab_c2_base.json 2>>gpurun_out/ab.err
-for v in w8nt2 w8nt4 w2nt4; do
-  KAFMM_LIB=$PWD/paper_2010_15155_b200/libkafmm_$v.so timeout 600 python bench.py --config 2 --no-cpu-baseline --no-e2e --steps 5 > gpurun_out/ab_c2_$v.json 2>>gpurun_out/ab.err
-done
-timeout 600 python bench.py --config 3 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c3_base.json 2>>gpurun_out/ab.err
-for v in w8nt2 w2nt4; do
-  KAFMM_LIB=$PWD/paper_2010_15155_b200/libkafmm_$v.so timeout 600 python bench.py --config 3 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c3_$v.json 2>>gpurun_out/ab.err
+# forward DFT: twiddle fragments in registers per pass (default) vs from L1 (nort)
+timeout 900 python -m pytest tests/test_gpu_m2l_modes.py -x -q > gpurun_out/ab_pytest.log 2>&1; echo pytest=$?; tail -1 gpurun_out/ab_pytest.log
+for c in 2 4 5; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c${c}_rt.json 2>>gpurun_out/ab.err
+  KAFMM_LIB=$PWD/paper_2010_15155_b200/libkafmm_nort.so timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c${c}_nort.json 2>>gpurun_out/ab.err
 done
