@@ -592,13 +592,13 @@ static bool chunk_uses_pairs(const Plan& Pl, const FftChunk& ch) {
   return Pl.m2l_mode == M2L_FFT_PAIRS || (Pl.m2l_mode == M2L_FFT && ch.block_fill < pair_fill_threshold());
 }
 
-// transforms per forward CTA: 2 at p <= 10 (measured after the z pass started reading UE
-// directly: C2 M2L transforms 3.5 -> 2.8 ms, nb 1 / 4 slower, profiles/r01_fft_rework_ab.txt),
-// 1 above; KAFMM_FWD_NB=1|2|4 overrides (tuning knob)
-static int fwd_nb(int p) {
+// transforms per forward CTA: 2 (measured after the z pass started reading UE directly:
+// C2 M2L transforms 3.5 -> 2.8 ms with nb 1 / 4 slower, profiles/r01_fft_rework_ab.txt;
+// C4 (p = 12) 206 -> 177 ms against 1); KAFMM_FWD_NB=1|2|4 overrides (tuning knob)
+static int fwd_nb(int) {
   static const char* e = getenv("KAFMM_FWD_NB");
   if (e) return atoi(e) >= 4 ? 4 : (atoi(e) >= 2 ? 2 : 1);
-  return p <= 10 ? 2 : 1;
+  return 2;
 }
 
 template <int P>
