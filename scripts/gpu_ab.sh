@@ -1,3 +1,1 @@
-# launch list of the bench command itself (C2), after it ran plain
-timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bl_plain.json 2>/dev/null; echo plain=$?
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bl_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bl_ncu.log 2>&1; echo ncu=$?
+timeout 1200 python -m pytest tests/test_gpu_m2l_modes.py -q > gpurun_out/modes.log 2>&1; echo pytest=$?; tail -3 gpurun_out/modes.log

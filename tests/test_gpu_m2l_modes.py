@@ -22,7 +22,10 @@ def _clustered(n, seed):
 CASES = [("stokeslet", lambda: _clustered(6000, 31), 6, 30),
          ("laplace_pgrad", lambda: np.random.default_rng(32).random((20000, 3)), 8, 40),
          ("rpy", lambda: WL.make_points(WL.CONFIGS[5], 9000, n_spheres=40), 5, 40),
-         ("stokes_reg_vel", lambda: _clustered(5000, 33), 12, 40)]
+         ("stokes_reg_vel", lambda: _clustered(5000, 33), 12, 40),
+         ("laplace_pgradgrad", lambda: _clustered(6000, 34), 4, 30),
+         ("stokes_reg_vel_omega", lambda: _clustered(5000, 35), 7, 40),
+         ("laplace_qpgradgrad", lambda: np.random.default_rng(36).random((8000, 3)), 3, 30)]
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
