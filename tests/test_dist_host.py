@@ -119,9 +119,9 @@ def _gloo_rank(rank, world, port, pts, vals, q):
         dist.destroy_process_group()
 
 
-def test_spmd_eval_gloo_world2_equals_oracle(setup):
+@pytest.mark.parametrize("world", [2, 4])
+def test_spmd_eval_gloo_equals_oracle(setup, world):
     pts, vals, _, _, _, ref = setup
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
