@@ -34,6 +34,7 @@ static T* h2d(Plan& P, const std::vector<T>& h) {
 // M2L (dense) tiles from the V pairs whose target is active; the pairs are
 // sorted by (level, offset), so filtering keeps the runs that share an operator.
 void build_m2l_batch(Plan& P) {
+  free_batch(P, P.g_m2l);
   std::vector<int2> pr;
   std::vector<int32_t> lev, ijk;
   d2h(P, pr, P.d_v_pairs, P.n_v);

@@ -917,6 +917,10 @@ void build_fft_chunks(Plan& P, int64_t budget) {
     }
   }
   const int64_t per_block = (int64_t)R * P.NF * 16;  // one parent block of spectra
+  for (FftChunk& c : P.fft_chunks)  // re-planning (kafmm_restrict): release the old lists
+    for (void* p : {(void*)c.d_qbox, (void*)c.d_nbr, (void*)c.d_tbox, (void*)c.d_tpb, (void*)c.d_toff,
+                    (void*)c.d_tpb_pair, (void*)c.d_pl_off, (void*)c.d_pl})
+      dfree(P, p);
   P.fft_chunks.clear();
   P.fft_max_nq = P.fft_max_npar = 0;
   std::vector<int32_t> qlocal(P.nbox, -1);

@@ -40,6 +40,7 @@ struct GemmBatch {  // one launch of the grouped GEMM
   std::vector<GemmTile> h_tiles;
   GemmTile* d_tiles = nullptr;
   int2* d_items = nullptr;  // x = input column (box / leaf slot), y = output column
+  bool owns_items = true;   // false when d_items aliases another array (the V-pair list)
   int64_t n_items = 0;
   int ntiles() const { return (int)h_tiles.size(); }
 };
@@ -223,6 +224,7 @@ struct Plan {
   int64_t bytes = 0;
 
   std::vector<void*> allocs;
+  std::vector<int64_t> alloc_bytes;  // size of allocs[i] (plan byte count after dfree)
 };
 
 // error handling -----------------------------------------------------------
@@ -248,6 +250,7 @@ T* dalloc(Plan& P, size_t count) {
   KF_CUDA(cudaMalloc(&p, b));
   KF_CUDA(cudaMemsetAsync(p, 0, b, P.stream));
   P.allocs.push_back(p);
+  P.alloc_bytes.push_back((int64_t)b);
   P.bytes += (int64_t)b;
   return (T*)p;
 }
@@ -255,11 +258,19 @@ T* dalloc(Plan& P, size_t count) {
 // release a dalloc'ed buffer early (re-planning after kafmm_restrict)
 inline void dfree(Plan& P, void* p) {
   if (!p) return;
-  for (auto& a : P.allocs)
-    if (a == p) {
+  for (size_t i = 0; i < P.allocs.size(); ++i)
+    if (P.allocs[i] == p) {
       cudaFree(p);
-      a = nullptr;
+      P.allocs[i] = nullptr;
+      P.bytes -= P.alloc_bytes[i];
+      P.alloc_bytes[i] = 0;
     }
+}
+
+inline void free_batch(Plan& P, GemmBatch& g) {
+  dfree(P, g.d_tiles);
+  if (g.owns_items) dfree(P, g.d_items);
+  g = GemmBatch();
 }
 
 // event around an M2L product launch (stage timing only)

@@ -626,6 +626,7 @@ void build_tree_and_lists(Plan& P, const double* d_points) {
         }
         g.n_items = P.n_v;
         g.d_items = P.d_v_pairs;
+        g.owns_items = false;
         g.d_tiles = dalloc<GemmTile>(P, g.h_tiles.size());
         KF_CUDA(cudaMemcpyAsync(g.d_tiles, g.h_tiles.data(), g.h_tiles.size() * sizeof(GemmTile),
                                 cudaMemcpyHostToDevice, st));
@@ -723,6 +724,11 @@ static void tiles_for_runs(GemmBatch& g, const std::vector<int2>& items, const s
 }
 
 void build_gemm_batches(Plan& P) {
+  // re-planning (kafmm_restrict): release the previous batches' device lists
+  free_batch(P, P.g_uc2ue_1);
+  free_batch(P, P.g_uc2ue_2);
+  for (auto* v : {&P.g_m2m, &P.g_dc2de_1, &P.g_dc2de_2, &P.g_l2l})
+    for (GemmBatch& g : *v) free_batch(P, g);
   std::vector<int32_t> hlevel, hparent, hijk, hleaf_ids, hs2m;
   std::vector<uint8_t> hleaf;
   to_host(P, hlevel, P.d_level, P.nbox);
