@@ -2,7 +2,9 @@
 
 TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
 ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
-package.  The product path (``paper_2010_15155_b200``) never imports it and
+package (plus the developer check scripts under ``scripts/``, which compare the
+CUDA path with it the way the tests do, and ``scripts/make_golden.py``, which
+writes the golden files from it alone).  The product path (``paper_2010_15155_b200``) never imports it and
 shares no code with it: the two meet only at the seeded input generators in
 ``workloads/``.
 
