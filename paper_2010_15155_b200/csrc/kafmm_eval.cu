@@ -34,7 +34,8 @@ __device__ __forceinline__ void box_geom(const int32_t* __restrict__ level, cons
 
 // a1 ------------------------------------------------------------------------
 __global__ void k_gather(const double* __restrict__ vals, const double* __restrict__ pts,
-                         const int64_t* __restrict__ perm, int64_t n, int ks, int srec, double* __restrict__ rec) {
+                         const int64_t* __restrict__ perm, int64_t n, int ks, int srec, int sqcol,
+                         double* __restrict__ rec) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t u = perm[i];
@@ -45,6 +46,9 @@ __global__ void k_gather(const double* __restrict__ vals, const double* __restri
 #pragma unroll
   for (int c = 3; c < 12; ++c) r[c] = 0.0;
   for (int c = 0; c < ks; ++c) r[3 + c] = vals[u * ks + c];
+  // the radius b (RPY) or blob size eps (regularised kernels) enters every pair only
+  // squared: the record carries the square, formed once per source here
+  if (sqcol >= 0) r[3 + sqcol] *= r[3 + sqcol];
   double2* o = reinterpret_cast<double2*>(rec + (int64_t)srec * i);
 #pragma unroll
   for (int c = 0; c < 6; ++c)
@@ -411,7 +415,10 @@ static void eval_up_impl(Plan& P, const double* d_src) {
   const Jobs& J = P.J;
   P.launches = 0;
   mark(ST_GATHER);
-  k_gather<<<nblk(P.n), 256, 0, st>>>(d_src, P.d_pts, P.d_perm, P.n, P.ks, SREC, P.d_rec);
+  const int sqcol = P.kernel == KAFMM_RPY || P.kernel == KAFMM_STOKES_REG_VEL ? 3
+                    : P.kernel == KAFMM_STOKES_REG_VEL_OMEGA        ? 6
+                                                                    : -1;
+  k_gather<<<nblk(P.n), 256, 0, st>>>(d_src, P.d_pts, P.d_perm, P.n, P.ks, SREC, sqcol, P.d_rec);
   KF_CHECK_LAUNCH();
   P.launches++;
   // the near field needs only the gathered records: it runs on a side stream
