@@ -1,6 +1,6 @@
-# b^2 / eps^2 formed once per source in the gather (new) vs per pair (prev)
-timeout 1800 python -m pytest tests/test_gpu_parity.py tests/test_gpu_wall.py tests/test_gpu_edge.py tests/test_gpu_fullsize.py tests/test_gpu_m2l_modes.py -x -q > gpurun_out/ab_pytest.log 2>&1; echo pytest=$?; tail -1 gpurun_out/ab_pytest.log
-for c in 6 4; do
-  timeout 600 python bench.py --config $c --no-cpu-baseline --steps 3 > gpurun_out/ab_c${c}_new.json 2>>gpurun_out/ab.err
-  KAFMM_LIB=$PWD/paper_2010_15155_b200/libkafmm_prev.so timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/ab_c${c}_prev.json 2>>gpurun_out/ab.err
-done
+# round-end check on the final code: full GPU suite, smoke, default bench line
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/fin5_pytest.log 2>&1; echo pytest=$?; tail -1 gpurun_out/fin5_pytest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin5_smoke.log 2>&1; echo smoke=$?
+timeout 900 python bench.py > gpurun_out/fin5_bench_c2.json 2> gpurun_out/fin5_bench_c2.err; echo bench=$?
+timeout 900 python bench.py --config 6 --steps 3 --no-cpu-baseline > gpurun_out/fin5_bench_c6.json 2>> gpurun_out/fin5_bench_c2.err; echo bench6=$?
+timeout 900 python bench.py --config 3 --steps 3 --no-cpu-baseline > gpurun_out/fin5_bench_c3.json 2>> gpurun_out/fin5_bench_c2.err; echo bench3=$?
