@@ -43,6 +43,16 @@ def test_kept_counts_laplace_p10():
     assert op.up_kept == op.dn_kept == 426   # SURVEY.md §8(c) R2 (tau = 1e-12)
 
 
+@pytest.mark.parametrize("p,kept", [(10, 1279), (12, 1571)])
+def test_kept_counts_stokeslet_p10_p12(p, kept):
+    # tau = 1e-12 keeps 1279 (p = 10, C3) and 1571 (p = 12, C4) of 3M
+    op = O.Operators("G", p)
+    assert op.up_kept == op.dn_kept == kept
+    s = op.up_sigma / op.up_sigma[0]
+    # margin to the threshold: measured 0.0055 dex (1.3%) at p = 12, 0.006+ at p = 10
+    assert np.min(np.abs(np.log10(s) - np.log10(O.TAU))) > 0.005
+
+
 def test_kept_counts_stokeslet_p8():
     op = O.Operators("G", 8)
     assert op.up_kept == op.dn_kept == 875
