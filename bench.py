@@ -5,9 +5,10 @@
 
 Metric (BASELINE.json): FMM eval points/s = (N_S + N_T) / t_eval at fixed p.
 A step is one kafmm_eval (gather, S2M, UC2UE, M2M, M2L, S2L, DC2DE, L2L,
-L2T, M2T, P2P, scatter) over config C's synthetic cloud (default C2 =
-BASELINE configs[1], 1M points Laplace PGrad p=10 cap 64), inputs resident
-in HBM.  L2 is flushed (256 MiB write) before every timed step, outside the
+L2T, M2T, P2P, scatter) over config C's synthetic cloud (default C5 =
+BASELINE configs[4], 64M points on 10^4 sphere surfaces, Stokeslet p=8 cap
+128: the largest config, which fits one GPU, and the 1-GPU point of the
+BASELINE scaling curve), inputs resident in HBM.  L2 is flushed (256 MiB write) before every timed step, outside the
 timed interval; each step is bracketed by CUDA events on the plan's stream.
 "e2e" times kafmm_eval_host: pinned host values -> device, eval, -> host.
 
@@ -17,7 +18,10 @@ the ranks exchange source values, shared and ghost multipoles and outputs
 over NCCL (strong scaling).  Time = max over ranks.
 
 --impl reference times the CPU oracle (oracle/, test infrastructure) on a
-bounded sample of the same workload on the host cores (rank 0 only).
+bounded sample of the same workload on the host cores (rank 0 only): each
+step evaluates, with the unmodified oracle FMM, the points of a seeded set of
+whole octree boxes of the workload (their subtrees are exactly the boxes'
+subtrees of the full tree), and reports (N_S + N_T) / time of that sample.
 """
 from __future__ import annotations
 
@@ -47,12 +51,14 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="kafmm", choices=["kafmm", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist", action="store_true", help="use the partitioned (NCCL) path even at N=1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--sample-points", type=int, default=3000,
+                    help="points per oracle sample (cpu_baseline / --impl reference step)")
     return ap.parse_args()
 
 
@@ -119,78 +125,100 @@ def _oracle_ops(spec):
     return op
 
 
-def _oracle_sample(spec, pts, vals, n_leaves_sample, seed, tree, op):
-    from oracle import fmm as F
-    smp = F.sample_leaves(tree, 1, seed=seed)
-    rng = np.random.default_rng(seed)
-    leaves = tree.leaves()
-    smp = sorted(int(b) for b in rng.choice(leaves, size=min(n_leaves_sample, leaves.size), replace=False))
-    tm = {}
-    F.fmm(pts, vals, spec.kernel, spec.p, spec.cap, target_leaves=smp, tree=tree, ops=op, timings=tm)
-    return smp, tm
+def subbox_sample(spec, pts, target, seed):
+    """Seeded sample of the workload: the points of whole octree boxes.
 
-
-def oracle_sample_rate(spec, pts, vals, budget_s):
-    """Oracle throughput on a bounded sample of the workload (cpu_baseline).
-
-    One oracle call in sampled mode: the full upward pass (S2M, UC2UE, M2M
-    over every leaf and box) plus the downward pass and near field of a seeded
-    sample of whole leaves.  Full-eval time is extrapolated as
-    t_upward + t_downward * n_leaves / n_sample_leaves.  List building is
-    setup (like the GPU plan) and not counted.
+    Draw a point, take the deepest box of the full tree's quantisation that
+    contains it and holds >= `target` points, and if that box holds more than
+    4 x target, the Morton-consecutive run of its children (starting at the
+    drawn point's child) until >= target points.  Every chosen box has more
+    than `cap` points (target >= cap), so the oracle's tree over the sample
+    reproduces those boxes' subtrees of the full tree exactly (same levels,
+    same splits); what the sample lacks is the rest of the cloud, so its
+    boundary leaves see fewer U/V/W/X neighbours than in the full problem and
+    the oracle does less work per point than it would on the full workload.
     """
+    target = max(int(target), spec.cap + 1)
+    rng = np.random.default_rng(seed)
+    q = np.clip(np.floor(pts * float(1 << 21)).astype(np.int64), 0, (1 << 21) - 1)
+    i = int(rng.integers(pts.shape[0]))
+    sel, level = np.arange(pts.shape[0]), 0
+    for L in range(1, 21):
+        sub = sel[np.all((q[sel] >> (21 - L)) == (q[i] >> (21 - L)), axis=1)]
+        if sub.size < target:
+            break
+        sel, level = sub, L
+    if sel.size > 4 * target and level < 20:
+        sh = 20 - level
+        octs = ((q[sel] >> sh) & 1) @ np.array([4, 2, 1])
+        o0 = int(((q[i] >> sh) & 1) @ np.array([4, 2, 1]))
+        keep = []
+        for o in list(range(o0, 8)) + list(range(o0)):
+            keep.append(sel[octs == o])
+            if sum(k.size for k in keep) >= target:
+                break
+        sel = np.sort(np.concatenate(keep))
+    return sel, level
+
+
+def oracle_subbox_run(spec, pts, vals, target, seed, op):
+    """One unmodified oracle FMM evaluation over a sub-box sample; returns
+    (points in the sample, evaluation seconds = upward + downward pass, box level).
+    The oracle's tree and interaction lists are setup (like the GPU plan)."""
     from oracle import fmm as F
     from oracle.tree import Tree
-    t = Tree(pts, spec.cap)
+    sel, level = subbox_sample(spec, pts, target, seed)
+    p_s, v_s = pts[sel], vals[sel]
+    t = Tree(p_s, spec.cap)
+    tm = {}
+    F.fmm(p_s, v_s, spec.kernel, spec.p, spec.cap, tree=t, ops=op, timings=tm)
+    return sel.size, tm["upward"] + tm["downward"], level
+
+
+def oracle_sample_rate(spec, pts, vals, budget_s, target):
+    """cpu_baseline: the oracle on seeded sub-box samples until budget_s of evaluation time."""
     op = _oracle_ops(spec)
-    nl = t.leaves().size
-    smp, tm = _oracle_sample(spec, pts, vals, 16, 0, t, op)
-    n_trg = sum(t.pts[b].size for b in smp)
-    t_full = tm["upward"] + tm["downward"] * nl / len(smp)
+    npts, secs, runs, levels = 0, 0.0, 0, []
+    while secs < budget_s and runs < 64:
+        n_s, t_s, lev = oracle_subbox_run(spec, pts, vals, target, 7919 + runs, op)
+        npts += n_s
+        secs += t_s
+        levels.append(lev)
+        runs += 1
     cores = len(os.sched_getaffinity(0))
-    return dict(value=2 * spec.n / t_full, unit="points/s", cores=cores, kind="oracle",
-                sample=(f"oracle (numpy/scipy, {cores} host threads) on {spec.name}: full upward pass "
-                        f"{tm['upward']:.1f} s + downward pass and near field of {len(smp)} sampled leaves "
-                        f"({n_trg} targets) {tm['downward']:.2f} s, extrapolated to all {nl} leaves "
-                        f"= {t_full:.0f} s per eval"))
+    return dict(value=2 * npts / secs, unit="points/s", cores=cores, kind="oracle",
+                sample=(f"oracle (numpy/scipy, {cores} host threads), full FMM evaluation (upward + downward "
+                        f"pass, lists and operators as setup) of {runs} seeded samples of {spec.name}, each the "
+                        f"points of whole boxes of its octree (box levels {sorted(set(levels))}, >= {target} "
+                        f"points each, {npts} points in all) in {secs:.1f} s; a sample lacks the rest of the "
+                        f"cloud, so its boundary leaves do less near/far work than in the full problem"))
 
 
 def run_reference(args, spec, pts, vals, rank):
     if rank != 0:
         return
-    from oracle import fmm as F
-    from oracle.tree import Tree
-    t = Tree(pts, spec.cap)
     op = _oracle_ops(spec)
-    nl = t.leaves().size
-    per, ups = [], []
-    s, warm, steps = 0, args.warmup, args.steps
-    while s < warm + steps:
-        # a step = the oracle's upward pass + downward/near field of 4 sampled leaves,
-        # prorated to the full evaluation
-        smp, tm = _oracle_sample(spec, pts, vals, 4, 1000 + s, t, op)
-        if s >= warm:
-            per.append(tm["upward"] + tm["downward"] * nl / len(smp))
-            ups.append(tm["upward"])
-        if s == 0 and tm["upward"] * (warm + steps) > 120:
-            # keep the arm within a few minutes: the first call (which also builds the
-            # lazily cached M2L matrices) counts as the only warm-up step
-            warm, steps = 1, max(1, min(steps, int(120 // max(tm["upward"], 1.0))))
-        s += 1
-    args.warmup = warm
+    per, sizes = [], []
+    for s in range(args.warmup + args.steps):
+        # a step = one unmodified oracle evaluation of a seeded sub-box sample of the workload
+        n_s, t_s, _ = oracle_subbox_run(spec, pts, vals, args.sample_points, 1000 + s, op)
+        if s >= args.warmup:
+            per.append(t_s)
+            sizes.append(n_s)
+    value = 2 * sum(sizes) / sum(per)
     ms = 1e3 * statistics.mean(per)
-    value = 2 * spec.n / (ms * 1e-3)
     cores = len(os.sched_getaffinity(0))
+    sample = (f"per step: the unmodified oracle FMM (numpy/scipy, {cores} host threads) on a seeded sample of "
+              f"whole octree boxes of {spec.name} (>= {args.sample_points} points; mean {statistics.mean(sizes):.0f} "
+              f"points, upward + downward pass timed, lists and operators as setup); value = 2 x sampled points / "
+              f"time summed over the {len(per)} timed steps")
     line = {"impl": "reference", "metric": "FMM eval points/sec (N_S+N_T) at fixed p", "value": value,
             "unit": "points/s", "n_gpus": args.gpus, "steps": len(per), "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(spec), "kernel": spec.kernel, "n": spec.n, "p": spec.p,
                        "max_pts_per_leaf": spec.cap},
-            "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
-                             "sample": (f"per step: oracle upward pass (mean {statistics.mean(ups):.1f} s) + "
-                                        f"downward pass and near field of 4 sampled leaves, extrapolated to "
-                                        f"{nl} leaves")},
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -369,15 +397,24 @@ def main():
     peak_dmma = fp64_peak("dmma")
     peak_dfma = fp64_peak("dfma")
     achieved = m2l_flop / (prod_ms * 1e-3) / 1e12
-    traffic = None
+    # DRAM traffic of the product kernels: device counters exist only under ncu, so it is
+    # read from the committed `ncu --set full` capture of this config (named in
+    # traffic_source), summed over the product launches of one evaluation, or null
+    traffic, traffic_src = None, f"null: no ncu --set full capture of C{spec.cid}'s product kernels committed"
     tf = os.path.join(ROOT, "profiles", f"traffic_C{spec.cid}.json")
     if os.path.exists(tf):
         try:
             tj = json.load(open(tf))
             if tj.get("m2l_mode") == mode:
-                traffic = tj.get("m2l_dram_bytes_per_launch")
+                traffic = tj.get("m2l_dram_bytes_per_eval", tj.get("m2l_dram_bytes_per_launch"))
+                traffic_src = tj.get("source")
         except Exception:
             traffic = None
+    fs = plan.fft_stats() if mode.startswith("fft") else None
+    algo_bytes = None
+    if fs:
+        # ub read once + cb written once, per evaluation
+        algo_bytes = 16 * 8 * kml * nf * (fs["source_blocks"] + fs["target_parents"])
     p2p_flop = P2P_FLOPS[spec.kernel] * n_p2p_local
     stage_mean = {k: round(v, 4) for k, v in breakdown.items()}
 
@@ -394,6 +431,8 @@ def main():
                    "m2l": mode},
         "roofline": {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": peak_dmma,
                      "unit": "TFLOP/s", "frac": achieved / peak_dmma, "traffic": traffic,
+                     "traffic_source": traffic_src, "traffic_unit": "DRAM bytes per evaluation, product launches",
+                     "algorithmic_bytes": algo_bytes,
                      "peak_source": "measured in this run: DMMA.8x8x4 loop (kafmm_fp64_peak); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
                      "algorithmic": algo, "kernel_ms": prod_ms, "m2l_stage_ms": m2l_ms,
@@ -404,7 +443,7 @@ def main():
         "stages_ms": stage_mean,
         "stages_note": ("per-stage events of one extra evaluation with the stages serialised (the timed steps run "
                         "the near field concurrently with the far field)"),
-        "fft_m2l": plan.fft_stats() if mode.startswith("fft") else None,
+        "fft_m2l": fs,
         "cuda_graph": None if graph_ms is None else {"ms_per_step": graph_ms, "value": 2 * spec.n / (graph_ms * 1e-3)},
         "clocks": clocks,
         "gpu_launches": launches,
@@ -413,7 +452,8 @@ def main():
                   "note": "kafmm_setup (tree, lists, operators, FFT tables) wall clock, rank 0; not part of value"},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = {k: v for k, v in oracle_sample_rate(spec, spec_pts, vals, args.cpu_budget).items()
+        line["cpu_baseline"] = {k: v for k, v in oracle_sample_rate(spec, spec_pts, vals, args.cpu_budget,
+                                                                    args.sample_points).items()
                                 if k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)

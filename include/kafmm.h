@@ -37,7 +37,7 @@ typedef struct kafmm_plan_s* kafmm_plan; /* opaque; owned by the library */
 
 typedef enum {
   KAFMM_OK = 0,
-  KAFMM_EINVAL = 1,     /* null pointer, n < 1, n > 2^31-1, p < 2, max_pts < 1, unknown kernel */
+  KAFMM_EINVAL = 1,     /* null pointer, n < 1, n > 2^31-1, p < 2 or p > 14, max_pts < 1, unknown kernel */
   KAFMM_EDOMAIN = 2,    /* a point outside [0,1)^3 */
   KAFMM_ENONFINITE = 3, /* NaN/Inf in points or values, or negative b / eps */
   KAFMM_ENOMEM = 4,     /* device allocation failed */
@@ -84,7 +84,9 @@ kafmm_status kafmm_kernel_dims(int kernel, int* k_s, int* k_t);
  *   points            device, n x 3 (x, y, z), every coordinate in [0, 1)
  *   n                 number of points (>= 1)
  *   kernel            a kafmm_kernel value
- *   p                 multipole order m of the paper, >= 2
+ *   p                 multipole order m of the paper, 2 <= p <= 14 (M = 6(p-1)^2+2 <= 1024 surface
+ *                     points, the leaf kernels' limit); the FFT M2L covers p = 3..8, 10, 12, other
+ *                     orders use the dense M2L
  *   max_pts_per_leaf  leaf capacity, >= 1
  *   out               receives the plan (NULL on failure)
  * Synchronous: returns after the plan is complete. */

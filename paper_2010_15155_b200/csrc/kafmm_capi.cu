@@ -103,6 +103,10 @@ kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int
     set_error("kafmm_setup: invalid argument");
     return KAFMM_EINVAL;
   }
+  if (6 * (p - 1) * (p - 1) + 2 > KAFMM_MAX_SURFACE) {  // the leaf kernels stage one surface per CTA
+    set_error("kafmm_setup: p too large (surface of 6(p-1)^2+2 points exceeds 1024; p <= 14)");
+    return KAFMM_EINVAL;
+  }
   kafmm_plan_s* P = nullptr;
   KF_API_BEGIN
   int dev = 0;
@@ -238,8 +242,14 @@ kafmm_status kafmm_setup2(const double* src_points, int64_t n_src, const double*
     set_error("kafmm_setup2: out of memory");
     return KAFMM_ENOMEM;
   }
-  cudaMemcpy(u, src_points, (size_t)n_src * 24, cudaMemcpyDeviceToDevice);
-  cudaMemcpy(u + 3 * n_src, trg_points, (size_t)n_trg * 24, cudaMemcpyDeviceToDevice);
+  if (cudaMemcpy(u, src_points, (size_t)n_src * 24, cudaMemcpyDeviceToDevice) != cudaSuccess ||
+      cudaMemcpy(u + 3 * n_src, trg_points, (size_t)n_trg * 24, cudaMemcpyDeviceToDevice) != cudaSuccess) {
+    const cudaError_t e = cudaGetLastError();
+    cudaFree(u);
+    set_error(std::string("kafmm_setup2: copying the point sets failed (device pointers of n x 3 doubles "
+                          "expected): ") + cudaGetErrorString(e));
+    return KAFMM_EINVAL;
+  }
   kafmm_status st = kafmm_setup(u, n_src + n_trg, kernel, p, max_pts_per_leaf, out);
   cudaFree(u);
   if (st != KAFMM_OK) return st;

@@ -155,6 +155,12 @@ void restrict_plan(Plan& P, int64_t plo, int64_t phi) {
   if (P.n_v > 0) build_m2l_batch(P);
   build_fft_chunks(P, P.fft_budget);
   P.restricted = true;
+  // the work lists, GEMM batches and FFT chunk buffers were rebuilt: a graph captured
+  // before must not be replayed (it points at the released lists)
+  if (P.gexec) KF_CUDA(cudaGraphExecDestroy(P.gexec));
+  P.gexec = nullptr;
+  P.g_src = nullptr;
+  P.g_out = nullptr;
 }
 
 // ---------------------------------------------------------------------------

@@ -603,8 +603,8 @@ static int fwd_nb(int) {
 
 template <int P>
 static void set_smem_attrs() {
-  static bool done = false;
-  if (done) return;
+  static std::atomic<uint64_t> done{0};
+  if (!first_on_device(done)) return;
   KF_CUDA(cudaFuncSetAttribute(k_fft_fwd<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)FwdCfg<P>::template smem<1>()));
   if (FwdCfg<P>::template smem<2>() <= 227 * 1024)
@@ -615,7 +615,6 @@ static void set_smem_attrs() {
                                  (int)FwdCfg<P>::template smem<4>()));
   KF_CUDA(cudaFuncSetAttribute(k_fft_inv<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)FftDims<P>::INV_SMEM));
-  done = true;
 }
 
 template <int P, int NB>
@@ -680,13 +679,12 @@ void run_m2l_fft(Plan& Pl) {
       const int ngrp = (ntb + PF_TB - 1) / PF_TB, nfb = (int)((Pl.NF + PFB - 1) / PFB);
       const unsigned grid = (unsigned)((int64_t)ngrp * nfb);
       const size_t smem = (size_t)N_HALF * (Pl.kml == 1 ? 1 : 6) * PFB * sizeof(double2);
-      static bool attr = false;
-      if (!attr) {
+      static std::atomic<uint64_t> attr{0};
+      if (first_on_device(attr)) {
         KF_CUDA(cudaFuncSetAttribute(k_m2l_pairsf<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(N_HALF * PFB * sizeof(double2))));
         KF_CUDA(cudaFuncSetAttribute(k_m2l_pairsf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(N_HALF * 6 * PFB * sizeof(double2))));
-        attr = true;
       }
       if (Pl.kml == 1)
         k_m2l_pairsf<1><<<grid, PF_THREADS, smem, Pl.stream>>>(ch.nt, ch.nq, ntb, (int)Pl.NF, Pl.d_that, Pl.d_ub,

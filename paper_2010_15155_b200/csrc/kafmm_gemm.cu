@@ -153,12 +153,11 @@ __global__ void __launch_bounds__(THREADS, 2)
 void launch_gemm(Plan& P, const GemmBatch& g, const double* A, int M, int K, int lda, const double* B, int ldb,
                  double* C, int ldc, int mode) {
   if (g.ntiles() == 0) return;
-  static bool init = false;
-  if (!init) {
+  static std::atomic<uint64_t> init{0};
+  if (first_on_device(init)) {
     KF_CUDA(cudaFuncSetAttribute(k_gemm_dmma<GEMM_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
     KF_CUDA(cudaFuncSetAttribute(k_gemm_dmma<GEMM_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
     KF_CUDA(cudaFuncSetAttribute(k_gemm_dmma<GEMM_ATOMIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
-    init = true;
   }
   if (K % BK != 0 || lda % 2 != 0 || ldb % 2 != 0) throw Error{KAFMM_EINVAL, "gemm: bad padding"};
   dim3 grid((unsigned)(((M + BM - 1) / BM) * (int64_t)g.ntiles()));

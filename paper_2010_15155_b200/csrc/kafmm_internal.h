@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <cstdlib>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -18,6 +19,15 @@ namespace kafmm {
 constexpr int QBITS = 21;
 constexpr int MAX_LEVEL = 20;
 constexpr int N_OFFSETS = 316;  // {-3..3}^3 minus {-1..1}^3 (V-list offsets)
+// Function attributes (large dynamic shared memory) are per device: true the first
+// time this is called for the current device with this flag word (thread-safe).
+inline bool first_on_device(std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  return !(done.fetch_or(bit) & bit);
+}
+constexpr int KAFMM_MAX_SURFACE = 1024;  // surface points per box the leaf kernels support (p <= 14)
 
 // Surface radii in units of the box half-width (reading R1).
 constexpr double ALPHA_UE = 1.05, ALPHA_UC = 2.95, ALPHA_DC = 1.05, ALPHA_DE = 2.95;

@@ -23,6 +23,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "kafmm_internal.h"
@@ -121,29 +124,65 @@ void build_operators(Plan& P) {
   KF_CUDA(cudaMemcpyAsync(P.d_surf, u.data(), u.size() * 8, cudaMemcpyHostToDevice, st));
 
   const double h0 = 0.5, c0[3] = {0.5, 0.5, 0.5};
-  // K(uc <- ue) at level 0, dense n x n (no padding) for the SVD
-  double *K, *UA, *VTA, *S, *work;
-  int* info;
-  KF_CUDA(cudaMallocAsync(&K, (size_t)n * n * 8, st));
+  // K(uc <- ue) at level 0, dense n x n (no padding) for the SVD.  The factors depend
+  // only on (ML kernel, p), so the process keeps one host copy per pair and later
+  // plans upload it instead of re-running gesvd (setup only; the SVD is hundreds of
+  // small solver launches)
+  double *UA, *VTA, *S;
   KF_CUDA(cudaMallocAsync(&UA, (size_t)n * n * 8, st));
   KF_CUDA(cudaMallocAsync(&VTA, (size_t)n * n * 8, st));
   KF_CUDA(cudaMallocAsync(&S, (size_t)n * 8, st));
-  KF_CUDA(cudaMallocAsync(&info, 8, st));
-  fill(P, K, n, c0, ALPHA_UC * h0, c0, ALPHA_UE * h0);
-  cusolverDnHandle_t sh;
-  KF_CUSOLVER(cusolverDnCreate(&sh));
-  KF_CUSOLVER(cusolverDnSetStream(sh, st));
-  int lwork = 0;
-  KF_CUSOLVER(cusolverDnDgesvd_bufferSize(sh, n, n, &lwork));
-  KF_CUDA(cudaMallocAsync(&work, (size_t)lwork * 8 + 8, st));
-  KF_CUSOLVER(cusolverDnDgesvd(sh, 'A', 'A', n, n, K, n, S, UA, n, VTA, n, work, lwork, nullptr, info));
-  int hinfo = 0;
-  P.h_sigma.resize(n);
-  KF_CUDA(cudaMemcpyAsync(&hinfo, info, 4, cudaMemcpyDeviceToHost, st));
-  KF_CUDA(cudaMemcpyAsync(P.h_sigma.data(), S, n * 8, cudaMemcpyDeviceToHost, st));
-  KF_CUDA(cudaStreamSynchronize(st));
-  cusolverDnDestroy(sh);
-  if (hinfo != 0) throw Error{KAFMM_ECUDA, "gesvd did not converge: info " + std::to_string(hinfo)};
+  struct SvdHost {
+    std::vector<double> ua, vta, s;
+  };
+  static std::mutex svd_mu;
+  static std::map<std::pair<int, int>, SvdHost> svd_cache;
+  const std::pair<int, int> svd_key(P.kml, p);
+  bool cached = false;
+  {
+    std::lock_guard<std::mutex> lk(svd_mu);
+    auto it = svd_cache.find(svd_key);
+    if (it != svd_cache.end()) {
+      KF_CUDA(cudaMemcpyAsync(UA, it->second.ua.data(), (size_t)n * n * 8, cudaMemcpyHostToDevice, st));
+      KF_CUDA(cudaMemcpyAsync(VTA, it->second.vta.data(), (size_t)n * n * 8, cudaMemcpyHostToDevice, st));
+      KF_CUDA(cudaMemcpyAsync(S, it->second.s.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
+      P.h_sigma = it->second.s;
+      KF_CUDA(cudaStreamSynchronize(st));
+      cached = true;
+    }
+  }
+  if (!cached) {
+    double *K, *work;
+    int* info;
+    KF_CUDA(cudaMallocAsync(&K, (size_t)n * n * 8, st));
+    KF_CUDA(cudaMallocAsync(&info, 8, st));
+    fill(P, K, n, c0, ALPHA_UC * h0, c0, ALPHA_UE * h0);
+    cusolverDnHandle_t sh;
+    KF_CUSOLVER(cusolverDnCreate(&sh));
+    KF_CUSOLVER(cusolverDnSetStream(sh, st));
+    int lwork = 0;
+    KF_CUSOLVER(cusolverDnDgesvd_bufferSize(sh, n, n, &lwork));
+    KF_CUDA(cudaMallocAsync(&work, (size_t)lwork * 8 + 8, st));
+    KF_CUSOLVER(cusolverDnDgesvd(sh, 'A', 'A', n, n, K, n, S, UA, n, VTA, n, work, lwork, nullptr, info));
+    int hinfo = 0;
+    P.h_sigma.resize(n);
+    KF_CUDA(cudaMemcpyAsync(&hinfo, info, 4, cudaMemcpyDeviceToHost, st));
+    KF_CUDA(cudaMemcpyAsync(P.h_sigma.data(), S, n * 8, cudaMemcpyDeviceToHost, st));
+    KF_CUDA(cudaStreamSynchronize(st));
+    cusolverDnDestroy(sh);
+    KF_CUDA(cudaFreeAsync(K, st));
+    KF_CUDA(cudaFreeAsync(work, st));
+    KF_CUDA(cudaFreeAsync(info, st));
+    if (hinfo != 0) throw Error{KAFMM_ECUDA, "gesvd did not converge: info " + std::to_string(hinfo)};
+    SvdHost h;
+    h.ua.resize((size_t)n * n);
+    h.vta.resize((size_t)n * n);
+    h.s = P.h_sigma;
+    KF_CUDA(cudaMemcpy(h.ua.data(), UA, (size_t)n * n * 8, cudaMemcpyDeviceToHost));
+    KF_CUDA(cudaMemcpy(h.vta.data(), VTA, (size_t)n * n * 8, cudaMemcpyDeviceToHost));
+    std::lock_guard<std::mutex> lk(svd_mu);
+    svd_cache.emplace(svd_key, std::move(h));
+  }
   int kept = 0;
   for (int i = 0; i < n; ++i)
     if (P.h_sigma[i] > TAU * P.h_sigma[0]) ++kept;
@@ -188,12 +227,9 @@ void build_operators(Plan& P) {
   }
   KF_CUDA(cudaStreamSynchronize(st));
   cublasDestroy(bh);
-  KF_CUDA(cudaFreeAsync(K, st));
   KF_CUDA(cudaFreeAsync(UA, st));
   KF_CUDA(cudaFreeAsync(VTA, st));
   KF_CUDA(cudaFreeAsync(S, st));
-  KF_CUDA(cudaFreeAsync(work, st));
-  KF_CUDA(cudaFreeAsync(info, st));
   KF_CUDA(cudaFreeAsync(tmp, st));
   KF_CUDA(cudaFreeAsync(Kp, st));
   KF_CUDA(cudaStreamSynchronize(st));

@@ -7,7 +7,7 @@ import workloads as WL
 from oracle import fmm as F
 from paper_2010_15155_b200 import KAFMM, KafmmError
 
-from .gpu_helpers import run_gpu
+from .gpu_helpers import assert_parity, block_max_errors, run_gpu
 
 pytestmark = pytest.mark.gpu
 
@@ -38,7 +38,7 @@ def test_duplicate_points_and_zero_values(kernel):
     vals = WL.random_values(kernel, 1000, 5)
     plan, out = run_gpu(pts, vals, kernel, 6, 24)
     ref = F.fmm(pts, vals, kernel, 6, 24)["out"]
-    assert max(F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) for lo, hi in F.blocks(kernel)) <= 1e-10
+    assert_parity(kernel, out, ref)
     z = np.zeros_like(vals)
     if z.shape[1] == 4:
         z[:, 3] = vals[:, 3]
@@ -57,7 +57,7 @@ def test_points_on_cell_boundaries_and_max_depth():
     plan, out = run_gpu(pts, vals, "stokeslet", 5, 4)
     ref = F.fmm(pts, vals, "stokeslet", 5, 4)
     assert plan.info().depth == ref["tree"].depth == 20
-    assert F.rel_l2(out, ref["out"]) <= 1e-10
+    assert_parity("stokeslet", out, ref["out"])
 
 
 def test_invalid_inputs_fail_loudly():
@@ -108,8 +108,7 @@ def test_leaves_larger_than_one_thread_pass(kernel):
         again = plan.eval(src).cpu().numpy()
         assert F.rel_l2(again, out) < 1e-12
     ref = F.fmm(pts, vals, kernel, 5, 1100)["out"]
-    for lo, hi in F.blocks(kernel):
-        assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10
+    assert_parity(kernel, out, ref)
 
 
 @pytest.mark.parametrize("kernel", ["laplace_pgrad", "rpy"])
@@ -148,7 +147,7 @@ def test_cuda_graph_replay_matches_and_follows_inputs():
     a.copy_(torch.from_numpy(v2))           # same pointers, new values: the replay reads them
     plan.eval(a, out)
     ref2 = F.fmm(pts, v2, "stokeslet", 6, 40)["out"]
-    assert F.rel_l2(out.cpu().numpy(), ref2) <= 1e-10
+    assert_parity("stokeslet", out.cpu().numpy(), ref2)
     b = torch.from_numpy(v1).cuda()         # new pointer: re-captured
     assert F.rel_l2(plan.eval(b).cpu().numpy(), ref1) < 1e-12
     plan.set_graph(False)
@@ -166,8 +165,7 @@ def test_orders_outside_the_fft_set_and_tiny_orders(p):
     assert plan.m2l() == ("fft" if p == 3 else "dense")
     out = plan.eval(torch.from_numpy(vals).cuda()).cpu().numpy()
     ref = F.fmm(pts, vals, kernel, p, 30)["out"]
-    for lo, hi in F.blocks(kernel):
-        assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10
+    assert_parity(kernel, out, ref)
 
 
 @pytest.mark.parametrize("kernel", ["laplace_pgrad", "stokes_reg_vel_omega", "rpy"])
@@ -186,5 +184,4 @@ def test_separate_source_and_target_sets(kernel):
     if kernel in WL.PARAM_COL and kernel != "rpy":
         uv[4000:, WL.PARAM_COL[kernel]] = 1.0   # reading R19: blob size of zero-strength target rows
     ref = F.fmm(union, uv, kernel, 6, 32)["out"][4000:]
-    for lo, hi in F.blocks(kernel):
-        assert F.rel_l2(out[:, lo:hi], ref[:, lo:hi]) <= 1e-10
+    assert_parity(kernel, out, ref)

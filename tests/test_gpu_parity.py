@@ -14,7 +14,7 @@ from oracle import fmm as F
 from oracle import lists as OL
 from oracle.tree import Tree
 
-from .gpu_helpers import block_errors, oracle_tree_keyed, run_gpu, tree_keyed
+from .gpu_helpers import assert_parity, block_errors, oracle_tree_keyed, run_gpu, tree_keyed
 
 pytestmark = pytest.mark.gpu
 
@@ -102,8 +102,7 @@ def test_kept_counts(case):
 
 
 def test_fmm_parity_with_oracle(case):
-    errs = block_errors(case["kernel"], case["gpu"], case["ref"]["out"])
-    assert max(errs) <= TOL, errs
+    assert_parity(case["kernel"], case["gpu"], case["ref"]["out"], l2_tol=TOL)
 
 
 def test_error_vs_direct_within_2x_oracle(case):
