@@ -12,7 +12,7 @@ python scripts/launch_summary.py gpurun_out/a_launches_c5.csv > gpurun_out/a_lau
 timeout 1200 ncu -f --set full --clock-control none --import-source on -k regex:k_m2l_ -c 18 -o /tmp/a_prod \
   python scripts/profile_eval.py 5 1 > gpurun_out/a_ncu_prod.log 2>&1; echo ncu_prod=$?
 python scripts/ncu_summary.py /tmp/a_prod.ncu-rep > gpurun_out/a_c5_prod_ncu.txt 2>&1
-timeout 1200 ncu -f --set full --clock-control none --import-source on -k regex:k_gemm_dmma -c 4 -o /tmp/a_gemm \
+timeout 1200 ncu -f --set full --clock-control none --import-source on -k regex:k_gemm_dmma -c 14 -o /tmp/a_gemm \
   python scripts/profile_eval.py 5 1 > gpurun_out/a_ncu_gemm.log 2>&1; echo ncu_gemm=$?
 python scripts/ncu_summary.py /tmp/a_gemm.ncu-rep > gpurun_out/a_c5_gemm_ncu.txt 2>&1
 cp /tmp/a_prod.ncu-rep gpurun_out/ 2>/dev/null
