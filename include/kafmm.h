@@ -102,7 +102,11 @@ kafmm_status kafmm_set_stream(kafmm_plan plan, void* stream);
  *   src_values  device, n x k_s, user (setup) order
  *   trg_out     device, n x k_t, user order, overwritten
  * Asynchronous on the plan's stream; trg_out is valid after stream sync.
- * A plan serves one evaluation at a time (single workspace). */
+ * A plan serves one evaluation at a time (single workspace).
+ * Input errors found on the device (a NaN/Inf source value, a negative b or eps)
+ * raise a sticky flag while the values are gathered; the next kafmm_sync (or
+ * kafmm_eval_host, which synchronises) returns KAFMM_ENONFINITE and clears it,
+ * so the hot path itself never waits on the host. */
 kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_out);
 
 /* End-to-end variant with HOST buffers: copies src_values host->device, runs
@@ -128,7 +132,9 @@ kafmm_status kafmm_eval2(kafmm_plan plan, const double* src_values, double* trg_
  * kafmm_eval itself does not check, to keep the hot path free of host syncs. */
 kafmm_status kafmm_check_values(kafmm_plan plan, const double* src_values);
 
-/* Waits for the plan's stream; surfaces asynchronous CUDA errors. */
+/* Waits for the plan's stream; surfaces asynchronous CUDA errors, and
+ * KAFMM_ENONFINITE if an evaluation since the last sync saw a non-finite source
+ * value or a negative b / eps (the outputs of that evaluation are then undefined). */
 kafmm_status kafmm_sync(kafmm_plan plan);
 
 void kafmm_destroy(kafmm_plan plan);

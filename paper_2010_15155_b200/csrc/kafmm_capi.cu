@@ -314,6 +314,7 @@ kafmm_status kafmm_eval_host(kafmm_plan plan, const double* src_values, double* 
   run_eval(P, P.d_stage_in, P.d_stage_out);
   KF_CUDA(cudaMemcpyAsync(trg_out, P.d_stage_out, (size_t)P.n * P.kt * 8, cudaMemcpyDeviceToHost, P.stream));
   KF_CUDA(cudaStreamSynchronize(P.stream));
+  take_nonfinite(P);
   return KAFMM_OK;
   KF_API_END
 }
@@ -331,6 +332,7 @@ kafmm_status kafmm_sync(kafmm_plan plan) {
   KF_API_BEGIN
   KF_CUDA(cudaStreamSynchronize(plan->stream));
   KF_CUDA(cudaGetLastError());
+  take_nonfinite(*plan);
   return KAFMM_OK;
   KF_API_END
 }

@@ -35,7 +35,7 @@ __device__ __forceinline__ void box_geom(const int32_t* __restrict__ level, cons
 // a1 ------------------------------------------------------------------------
 __global__ void k_gather(const double* __restrict__ vals, const double* __restrict__ pts,
                          const int64_t* __restrict__ perm, int64_t n, int ks, int srec, int sqcol,
-                         double* __restrict__ rec) {
+                         double* __restrict__ rec, int* __restrict__ nonfinite) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t u = perm[i];
@@ -45,7 +45,13 @@ __global__ void k_gather(const double* __restrict__ vals, const double* __restri
   r[2] = pts[4 * i + 2];
 #pragma unroll
   for (int c = 3; c < 12; ++c) r[c] = 0.0;
-  for (int c = 0; c < ks; ++c) r[3 + c] = vals[u * ks + c];
+  bool bad = false;
+  for (int c = 0; c < ks; ++c) {
+    r[3 + c] = vals[u * ks + c];
+    bad |= !isfinite(r[3 + c]);
+  }
+  if (sqcol >= 0) bad |= r[3 + sqcol] < 0.0;
+  if (bad) atomicOr(nonfinite, 1);  // sticky; reported by kafmm_sync / kafmm_eval_host (ENONFINITE)
   // the radius b (RPY) or blob size eps (regularised kernels) enters every pair only
   // squared: the record carries the square, formed once per source here
   if (sqcol >= 0) r[3 + sqcol] *= r[3 + sqcol];
@@ -418,7 +424,7 @@ static void eval_up_impl(Plan& P, const double* d_src) {
   const int sqcol = P.kernel == KAFMM_RPY || P.kernel == KAFMM_STOKES_REG_VEL ? 3
                     : P.kernel == KAFMM_STOKES_REG_VEL_OMEGA        ? 6
                                                                     : -1;
-  k_gather<<<nblk(P.n), 256, 0, st>>>(d_src, P.d_pts, P.d_perm, P.n, P.ks, SREC, sqcol, P.d_rec);
+  k_gather<<<nblk(P.n), 256, 0, st>>>(d_src, P.d_pts, P.d_perm, P.n, P.ks, SREC, sqcol, P.d_rec, P.d_flag + 1);
   KF_CHECK_LAUNCH();
   P.launches++;
   // the near field needs only the gathered records: it runs on a side stream
@@ -530,6 +536,16 @@ void run_eval_down(Plan& P, double* d_out) {
 void run_eval(Plan& P, const double* d_src, double* d_out) {
   run_eval_up(P, d_src);
   run_eval_down(P, d_out);
+}
+
+// the sticky flag k_gather raises on a non-finite source value or a negative b / eps
+// (d_flag[1]); read and cleared by the synchronising entry points
+void take_nonfinite(Plan& P) {
+  int h = 0;
+  KF_CUDA(cudaMemcpyAsync(&h, P.d_flag + 1, 4, cudaMemcpyDeviceToHost, P.stream));
+  KF_CUDA(cudaMemsetAsync(P.d_flag + 1, 0, 4, P.stream));
+  KF_CUDA(cudaStreamSynchronize(P.stream));
+  if (h) throw Error{KAFMM_ENONFINITE, "non-finite source value or negative b/eps in an evaluation since the last sync"};
 }
 
 void check_values(Plan& P, const double* d_src) {

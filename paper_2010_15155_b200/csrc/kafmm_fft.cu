@@ -86,13 +86,6 @@ __global__ void k_spectra_transpose(int NF, int nc, const double2* __restrict__ 
 // ---------------------------------------------------------------------------
 // hot path kernels
 // ---------------------------------------------------------------------------
-// frequencies per target lane group of the per-pair product (k_m2l_pairsf), which is
-// also the frequency block of ub in per-pair chunks
-#ifndef KF_PAIR_FB
-#define KF_PAIR_FB 8
-#endif
-constexpr int PFB = KF_PAIR_FB;
-
 template <int P>
 struct FftDims {
   static constexpr int NG = 2 * P - 1, NZ = NG / 2 + 1, NF = NG * NG * NZ;
@@ -222,7 +215,7 @@ template <int P, int NB, int NBC>
 __device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* (&src)[NB], const int (&slot)[NB],
                                          const int16_t* __restrict__ lmap, int kml, double2* __restrict__ ub,
                                          int64_t nq, int64_t q, int R, const double* __restrict__ wz,
-                                         const double* __restrict__ wf, bool blocked) {
+                                         const double* __restrict__ wf, const int16_t* __restrict__ fpos) {
   using D = FftDims<P>;
   using S = DftShape<P>;
   constexpr int NG = D::NG, NZ = D::NZ, NGNZ = NG * NZ, PER = FwdCfg<P>::PER, PP = P * P, YO = 2 * PP * NZ;
@@ -258,9 +251,10 @@ __device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* 
       },
       [&](int L, int o, double2 v) {
         const int r = L / NBC, t = L - r * NBC, f = o * NGNZ + r, sl = pick<NB>(slot, t, NBC);
-        if (blocked)  // per-pair chunks: [f / PFB][q][R][f % PFB] (k_m2l_pairsf)
-          ub[(((int64_t)(f / PFB) * nq + q) * R + sl) * PFB + (f % PFB)] = v;
-        else
+        if (fpos) {  // sparse chunks: [group][q][R][slot] (k_m2l_sparse)
+          const int fp = __ldg(fpos + f);
+          ub[(((int64_t)(fp >> 5) * nq + q) * R + sl) * 32 + (fp & 31)] = v;
+        } else
           ub[((int64_t)f * nq + q) * R + sl] = v;
       });
 }
@@ -268,10 +262,10 @@ __device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* 
 template <int P, int NB, int NBC>
 __device__ __forceinline__ void fwd_dispatch(int nb, double* sm, const double* (&src)[NB], const int (&slot)[NB],
                                              const int16_t* lmap, int kml, double2* ub, int64_t nq, int64_t q, int R,
-                                             const double* wz, const double* wf, bool blocked) {
-  if (nb == NBC) fwd_body<P, NB, NBC>(sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf, blocked);
+                                             const double* wz, const double* wf, const int16_t* fpos) {
+  if (nb == NBC) fwd_body<P, NB, NBC>(sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf, fpos);
   else if constexpr (NBC > 1)
-    fwd_dispatch<P, NB, NBC - 1>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf, blocked);
+    fwd_dispatch<P, NB, NBC - 1>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf, fpos);
 }
 
 template <int P, int NB>
@@ -279,7 +273,7 @@ __global__ void __launch_bounds__(256)
     k_fft_fwd(const int32_t* __restrict__ qbox, const int32_t* __restrict__ child, int64_t nq,
               const double* __restrict__ ue, int ldn, int kml, const int16_t* __restrict__ lmap,
               double2* __restrict__ ub, int zero_missing, const double* __restrict__ wz,
-              const double* __restrict__ wf) {
+              const double* __restrict__ wf, const int16_t* __restrict__ fpos) {
   using D = FftDims<P>;
   constexpr int NF = D::NF;
   extern __shared__ __align__(16) double sm[];
@@ -315,7 +309,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   if (nb == 0) return;
-  fwd_dispatch<P, NB, NB>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf, !zero_missing);
+  fwd_dispatch<P, NB, NB>(nb, sm, src, slot, lmap, kml, ub, nq, q, R, wz, wf, zero_missing ? nullptr : fpos);
 }
 
 // inverse: one CTA per target box; its check spectrum cb[parent][b kml + a][f] (one contiguous row,
@@ -327,10 +321,10 @@ __global__ void __launch_bounds__(256)
     k_fft_inv(const int32_t* __restrict__ tbox, const int2* __restrict__ tpb, int64_t npar,
               const int32_t* __restrict__ level, const double2* __restrict__ cb, int kml,
               const int16_t* __restrict__ lat, int M, double* __restrict__ chk, int ldn,
-              const double* __restrict__ wi) {
+              const double* __restrict__ wi, const int16_t* __restrict__ fpos, int NFP) {
   using D = FftDims<P>;
   using S = DftShape<P>;
-  constexpr int NG = D::NG, NZ = D::NZ, NF = D::NF, NGNZ = NG * NZ;
+  constexpr int NG = D::NG, NZ = D::NZ, NGNZ = NG * NZ;
   extern __shared__ __align__(16) double sm[];
   double2* Dx = reinterpret_cast<double2*>(sm);  // [x][fy][fz]
   double2* E = Dx + P * NG * NZ;                 // [x][y][fz]
@@ -348,13 +342,13 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();
   for (int a = 0; a < kml; ++a) {
-    // target-major: one contiguous row
-    const double* col = reinterpret_cast<const double*>(cb + ((int64_t)pb.x * R + pb.y * kml + a) * NF);
+    // target-major: one contiguous row, frequency f at position fpos[f]
+    const double* col = reinterpret_cast<const double*>(cb + ((int64_t)pb.x * R + pb.y * kml + a) * NFP);
     dft_pass<S::KI, S::NIT>(  // x: lines (fy, fz), outputs x < P
         NGNZ, P, wi,
         [&](int line, int k) {
           const int fx = k >> 1;
-          return fx < NG ? __ldg(col + 2 * (fx * NGNZ + line) + (k & 1)) : 0.0;
+          return fx < NG ? __ldg(col + 2 * __ldg(fpos + fx * NGNZ + line) + (k & 1)) : 0.0;
         },
         [&](int line, int o, double2 v) { Dx[o * NGNZ + line] = v; });
     __syncthreads();
@@ -414,9 +408,9 @@ constexpr int DM_WARPS = KF_DM_WARPS;
 template <int KML, int NT>
 __global__ void __launch_bounds__(DM_WARPS * 32, KML == 1 ? KF_DMMA_MINB1 : KF_DMMA_MINB3)
     k_m2l_dmma(int64_t npar, int64_t nq, int npb, const double2* __restrict__ that, const double2* __restrict__ ub,
-               double2* __restrict__ cb, const int32_t* __restrict__ nbr, const int16_t* __restrict__ aidx) {
+               double2* __restrict__ cb, const int32_t* __restrict__ nbr, const int16_t* __restrict__ aidx,
+               const int16_t* __restrict__ fpos, int NFP) {
   constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML, KS = R / 4, PPW = NT * 8;
-  const int64_t NF = gridDim.x / npb;  // grid = parent blocks x frequency bins
   __shared__ double2 sT[N_OFFSETS * NC];
   const int64_t f = blockIdx.x / npb;
   const int pb = blockIdx.x % npb;
@@ -479,7 +473,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32, KML == 1 ? KF_DMMA_MINB1 : KF_D
       }
     }
   }
-  double2* cbf = cb + f;  // cb is target-major [parent][8 kml][NF]
+  double2* cbf = cb + fpos[f];  // cb is target-major [parent][8 kml][NFP], group-slot order
 #pragma unroll
   for (int m = 0; m < KML; ++m)
 #pragma unroll
@@ -489,100 +483,147 @@ __global__ void __launch_bounds__(DM_WARPS * 32, KML == 1 ? KF_DMMA_MINB1 : KF_D
         const int64_t Pn = P0 + n * 8 + 2 * tq + e;
         if (Pn < npar) {
           const double p1 = acc[m][n][0][e], p2 = acc[m][n][1][e];
-          cbf[(Pn * R + m * 8 + g) * NF] = make_double2(p1 - p2, acc[m][n][2][e] - p1 - p2);
+          cbf[(Pn * R + m * 8 + g) * NFP] = make_double2(p1 - p2, acc[m][n][2][e] - p1 - p2);
         }
       }
 }
 
-// The same product per V pair, for chunks whose parent blocks are mostly
-// empty (sparse adaptive trees).
-// The per-pair product with PFB consecutive frequencies per target: a warp is
-// 32/PFB targets x PFB frequencies (lane = PFB t + fi), so the lanes of a
-// target read one contiguous 16 PFB-byte run of operator spectra (SMEM) and of
-// source spectra (ub in the blocked layout [f / PFB][q][8 kml][f % PFB] that the
-// forward transform writes for these chunks) per pair and component, instead
-// of 16-B gathers at random banks / lines.  The operator spectra are even in
-// the offset (G(-r) = G(r) and the lattice differences are symmetric), so
-// T_{-o}(f) = conj T_o(f): SMEM holds the 158 offsets o < 158 ([c][o][PFB f]),
-// offset 315 - o is -o (the offset table is ordered lexicographically over a
-// symmetric set) and is read as the conjugate.  A CTA stages its frequencies'
-// spectra once and walks PF_TB target blocks.
-#ifndef KF_PF_THREADS
-#define KF_PF_THREADS 1024  // 32 warps per SM (registers allow no more)
-#endif
-constexpr int PF_THREADS = KF_PF_THREADS, PF_TPB = PF_THREADS / PFB, PF_TB = 8;
-constexpr int N_HALF = N_OFFSETS / 2;  // 158
+// The same product for chunks whose parent blocks are mostly empty (sparse
+// adaptive trees: points on surfaces), without the empty child slots.
+// A warp owns one target parent P for all 26 directions and 32 frequency bins
+// (lane = bin), so every branch on the occupancy of P's and its colleagues'
+// children is warp-uniform: absent (b, c) child pairs cost nothing.  For each
+// colleague Q_d and existing source child c the lane loads U_{Q_d, c}(f) once
+// (3 components, one 512-B run per warp) and applies it to every existing,
+// non-adjacent target child b:  C_b += T_{2d + c - b}(f) U_c  (9 complex
+// multiply-adds into registers, acc[8][kml]).
+// Operator spectra: a CTA holds 32 bins in shared memory, so the 316 offsets do
+// not fit (316 x 6 x 32 x 16 B = 970 KB).  The cube reflections shrink the
+// table: with S = diag(sx, sy, sz) the signs of o,
+//     T_o(f) = S [conj if sz < 0] T_|o|(R f) S,
+// R reflecting fx iff sx != sz and fy iff sy != sz (G(Rr) = S G(r) S; a
+// reflection of the lattice differences reflects the bin; T(-f) = conj T(f)
+// for the z axis of the half spectrum), so 56 offsets |o| suffice if a CTA's
+// bins are closed under (fx, fy) -> (+-fx, +-fy): the bins are grouped into
+// such orbits (build_fft_m2l), 32 per group, orbits never straddling an
+// 8-lane phase, so the reflected reads of a warp stay bank-conflict free.
+// Table: 56 x 6 x 32 x 16 B = 172 KB (Stokes family), 28 KB (Laplace).
+// c_pinfo[d][b][c]: base offset index (6 bits), reflection r (2 bits), conj
+// (1 bit) and the sign flips of the xy, xz, yz components (3 bits), or 0xFFFF
+// for an adjacent pair (not in the V list).
+constexpr int N_BASE = 56;
+constexpr int SP_WARPS = 12;  // 384 threads, one CTA per SM (172 KB table), <= 170 registers
+__constant__ uint16_t c_pinfo[26 * 64];
+
+__device__ __forceinline__ double xsign(double v, unsigned m) {  // flip the sign bit if m = 0x80000000
+  return __hiloint2double(__double2hiint(v) ^ (int)m, __double2loint(v));
+}
 
 template <int KML>
-__global__ void __launch_bounds__(PF_THREADS)
-    k_m2l_pairsf(int64_t nt, int64_t nq, int ntb, int NF, const double2* __restrict__ that,
-                 const double2* __restrict__ ub, double2* __restrict__ cb, const int2* __restrict__ tpb,
-                 const int64_t* __restrict__ off, const int32_t* __restrict__ pl) {
-  constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML, CS = N_HALF * PFB;
-  extern __shared__ double2 sTh[];  // [NC][N_HALF][PFB]
-  const int ngrp = (ntb + PF_TB - 1) / PF_TB;
-  const int fb = blockIdx.x / ngrp, grp = blockIdx.x % ngrp;
-  for (int i = threadIdx.x; i < N_HALF * NC * PFB; i += PF_THREADS) {
-    const int fi = i % PFB, oc = i / PFB, c = oc / N_HALF, o = oc - c * N_HALF;
-    const int f = fb * PFB + fi;
-    sTh[i] = f < NF ? that[((int64_t)f * N_OFFSETS + o) * NC + c] : make_double2(0.0, 0.0);
+__global__ void __launch_bounds__(SP_WARPS * 32, 1)
+    k_m2l_sparse(int64_t npar, int64_t nq, int NFP, const double2* __restrict__ tbase, const int* __restrict__ rslot,
+                 const double2* __restrict__ ub, double2* __restrict__ cb, const int32_t* __restrict__ nbr,
+                 const uint8_t* __restrict__ tpat, const uint8_t* __restrict__ qpat) {
+  constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
+  extern __shared__ __align__(16) double2 sTb[];  // [N_BASE][NC][32]
+  const int g = blockIdx.y;
+  {
+    const double4* src = reinterpret_cast<const double4*>(tbase + (int64_t)g * N_BASE * NC * 32);
+    double4* dst = reinterpret_cast<double4*>(sTb);
+    for (int i = threadIdx.x; i < N_BASE * NC * 16; i += SP_WARPS * 32) dst[i] = src[i];
   }
   __syncthreads();
-  const int fi = threadIdx.x % PFB, f = fb * PFB + fi;
-  const double2* ubb = ub + (int64_t)fb * nq * R * PFB + fi;
-  const double2* sTf = sTh + fi;
-  for (int tb = grp * PF_TB; tb < min(ntb, (grp + 1) * PF_TB); ++tb) {
-    const int64_t t = (int64_t)tb * PF_TPB + threadIdx.x / PFB;
-    if (t >= nt) break;
-    double2 acc[KML];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rs = rslot[g * 32 + lane];
+  const double2* ubg = ub + (int64_t)g * nq * R * 32 + lane;
+  for (int64_t P = (int64_t)blockIdx.x * SP_WARPS + warp; P < npar; P += (int64_t)gridDim.x * SP_WARPS) {
+    const unsigned bm = tpat[P];
+    if (!bm) continue;
+    double2 acc[8][KML];
 #pragma unroll
-    for (int a = 0; a < KML; ++a) acc[a] = make_double2(0.0, 0.0);
-    const int64_t e1 = off[t + 1];
-    for (int64_t e = off[t]; e < e1; e += 4) {  // lists padded with -1 to multiples of 4
-      const int4 v4 = *reinterpret_cast<const int4*>(pl + e);
-      const int v[4] = {v4.x, v4.y, v4.z, v4.w};
-      double2 u[4][KML];
+    for (int b = 0; b < 8; ++b)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double2* up = ubb + (int64_t)(v[j] >> 9) * KML * PFB;
+      for (int a = 0; a < KML; ++a) acc[b][a] = make_double2(0.0, 0.0);
+    for (int d = 0; d < 26; ++d) {
+      const int q = nbr[P * 26 + d];
+      if (q < 0) continue;
+      unsigned cm = qpat[q];
+      if (!cm) continue;
+      const double2* uq = ubg + (int64_t)q * R * 32;
+      const uint16_t* inf = c_pinfo + d * 64;
+      int c = __ffs(cm) - 1;
+      double2 U[KML];
 #pragma unroll
-        for (int a = 0; a < KML; ++a) u[j][a] = v[j] >= 0 ? up[a * PFB] : make_double2(0.0, 0.0);
-      }
+      for (int e = 0; e < KML; ++e) U[e] = uq[(c * KML + e) * 32];
+      while (true) {
+        cm &= cm - 1;
+        const int cn = cm ? __ffs(cm) - 1 : -1;
+        double2 Un[KML];
+        if (cn >= 0) {  // next source child's spectra in flight during this one's products
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int o = v[j] >= 0 ? (v[j] & 511) : 0;
-        const bool cj = o >= N_HALF;
-        const int oo = (cj ? N_OFFSETS - 1 - o : o) * PFB;
-        const double sg = cj ? -1.0 : 1.0;
-        auto T = [&](int c) {
-          const double2 t = sTf[c * CS + oo];
-          return make_double2(t.x, sg * t.y);
-        };
-        if (KML == 1) {
-          cmac(acc[0], T(0), u[j][0]);
-        } else {
-          const double2 t0 = T(0), t1 = T(1), t2 = T(2), t3 = T(NC > 3 ? 3 : 0), t4 = T(NC > 4 ? 4 : 0),
-                        t5 = T(NC > 5 ? 5 : 0);
-          const double2 u0 = u[j][0], u1 = u[j][KML > 1 ? 1 : 0], u2 = u[j][KML > 2 ? 2 : 0];
-          cmac(acc[0], t0, u0);
-          cmac(acc[0], t1, u1);
-          cmac(acc[0], t2, u2);
-          cmac(acc[KML > 1 ? 1 : 0], t1, u0);
-          cmac(acc[KML > 1 ? 1 : 0], t3, u1);
-          cmac(acc[KML > 1 ? 1 : 0], t4, u2);
-          cmac(acc[KML > 2 ? 2 : 0], t2, u0);
-          cmac(acc[KML > 2 ? 2 : 0], t4, u1);
-          cmac(acc[KML > 2 ? 2 : 0], t5, u2);
+          for (int e = 0; e < KML; ++e) Un[e] = uq[(cn * KML + e) * 32];
         }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          if (!((bm >> b) & 1u)) continue;
+          const unsigned info = inf[b * 8 + c];
+          if (info == 0xFFFFu) continue;
+          const int slot = (rs >> (5 * ((info >> 6) & 3))) & 31;
+          const double2* t = sTb + (info & 63) * NC * 32 + slot;
+          const unsigned mc = ((info >> 8) & 1u) << 31;  // conj: flip imaginary parts
+          if (KML == 1) {
+            const double2 t0 = t[0];
+            cmac(acc[b][0], make_double2(t0.x, xsign(t0.y, mc)), U[0]);
+          } else {
+            const unsigned mxy = ((info >> 9) & 1u) << 31, mxz = ((info >> 10) & 1u) << 31,
+                           myz = ((info >> 11) & 1u) << 31;
+            double2 T[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) T[k] = t[k * 32];
+            T[0].y = xsign(T[0].y, mc);
+            T[3].y = xsign(T[3].y, mc);
+            T[5].y = xsign(T[5].y, mc);
+            T[1] = make_double2(xsign(T[1].x, mxy), xsign(T[1].y, mxy ^ mc));
+            T[2] = make_double2(xsign(T[2].x, mxz), xsign(T[2].y, mxz ^ mc));
+            T[4] = make_double2(xsign(T[4].x, myz), xsign(T[4].y, myz ^ mc));
+            double2* o = acc[b];
+            cmac(o[0], T[0], U[0]);
+            cmac(o[0], T[1], U[KML > 1 ? 1 : 0]);
+            cmac(o[0], T[2], U[KML > 2 ? 2 : 0]);
+            cmac(o[KML > 1 ? 1 : 0], T[1], U[0]);
+            cmac(o[KML > 1 ? 1 : 0], T[3], U[KML > 1 ? 1 : 0]);
+            cmac(o[KML > 1 ? 1 : 0], T[4], U[KML > 2 ? 2 : 0]);
+            cmac(o[KML > 2 ? 2 : 0], T[2], U[0]);
+            cmac(o[KML > 2 ? 2 : 0], T[4], U[KML > 1 ? 1 : 0]);
+            cmac(o[KML > 2 ? 2 : 0], T[5], U[KML > 2 ? 2 : 0]);
+          }
+        }
+        if (cn < 0) break;
+        c = cn;
+#pragma unroll
+        for (int e = 0; e < KML; ++e) U[e] = Un[e];
       }
     }
-    if (f < NF) {
-      const int2 pb = tpb[t];
-      double2* o = cb + ((int64_t)pb.x * R + pb.y * KML) * NF + f;
+    double2* o = cb + (P * R) * (int64_t)NFP + g * 32 + lane;
 #pragma unroll
-      for (int a = 0; a < KML; ++a) o[(int64_t)a * NF] = acc[a];
-    }
+    for (int b = 0; b < 8; ++b)
+      if ((bm >> b) & 1u) {
+#pragma unroll
+        for (int a = 0; a < KML; ++a) o[(int64_t)(b * KML + a) * NFP] = acc[b][a];
+      }
   }
+}
+
+// base table of the sparse product: tbase[g][ob][c][s] = That_{o(ob)}(f(g, s))[c] (0 on padding slots)
+__global__ void k_tbase(int nfg, int nc, const int32_t* __restrict__ gfreq, const int16_t* __restrict__ boff,
+                        const double2* __restrict__ that, double2* __restrict__ tbase) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // over [nfg][56][nc][32]
+  if (t >= (int64_t)nfg * N_BASE * nc * 32) return;
+  const int s = (int)(t % 32);
+  const int64_t r = t / 32;
+  const int c = (int)(r % nc), ob = (int)((r / nc) % N_BASE), g = (int)(r / nc / N_BASE);
+  const int f = gfreq[g * 32 + s];
+  tbase[t] = f >= 0 ? that[((int64_t)f * N_OFFSETS + boff[ob]) * nc + c] : make_double2(0.0, 0.0);
 }
 
 // ---------------------------------------------------------------------------
@@ -622,7 +663,7 @@ static void launch_fwd_nb(Plan& Pl, const FftChunk& ch) {
   const int ng = (8 * Pl.kml + NB - 1) / NB;
   k_fft_fwd<P, NB><<<(unsigned)(ch.nq * ng), 256, FwdCfg<P>::template smem<NB>(), Pl.stream>>>(
       ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lmap, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1,
-      Pl.d_wz, Pl.d_wf);
+      Pl.d_wz, Pl.d_wf, Pl.d_fpos);
 }
 
 template <int P>
@@ -640,7 +681,8 @@ template <int P>
 static void launch_inv(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
   k_fft_inv<P><<<(unsigned)ch.nt, 256, FftDims<P>::INV_SMEM, Pl.stream>>>(
-      ch.d_tbox, ch.d_tpb, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn, Pl.d_wi);
+      ch.d_tbox, ch.d_tpb, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn, Pl.d_wi,
+      Pl.d_fpos, Pl.NFP);
   KF_CHECK_LAUNCH();
   Pl.launches++;
 }
@@ -673,25 +715,26 @@ void run_m2l_fft(Plan& Pl) {
     const bool pairs = chunk_uses_pairs(Pl, ch);
     prod_mark(Pl);
     if (pairs) {
-      // PFB frequencies per target (blocked ub layout; a thread per (target, frequency) with
-      // 16-B gathers measured 1163 ms on C5, profiles/r01_pairs4_ab.txt)
-      const int ntb = (int)((ch.nt + PF_TPB - 1) / PF_TPB);
-      const int ngrp = (ntb + PF_TB - 1) / PF_TB, nfb = (int)((Pl.NF + PFB - 1) / PFB);
-      const unsigned grid = (unsigned)((int64_t)ngrp * nfb);
-      const size_t smem = (size_t)N_HALF * (Pl.kml == 1 ? 1 : 6) * PFB * sizeof(double2);
+      // warp per target parent, 32 bins per CTA (group), parents strided over the CTAs
+      // of a group; the grid's x extent keeps every CTA on >= 16 parents per warp so the
+      // 172 KB table stage is amortised
+      const int NC = Pl.kml == 1 ? 1 : 6;
+      const size_t smem = (size_t)N_BASE * NC * 32 * sizeof(double2);
       static std::atomic<uint64_t> attr{0};
       if (first_on_device(attr)) {
-        KF_CUDA(cudaFuncSetAttribute(k_m2l_pairsf<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(N_HALF * PFB * sizeof(double2))));
-        KF_CUDA(cudaFuncSetAttribute(k_m2l_pairsf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(N_HALF * 6 * PFB * sizeof(double2))));
+        KF_CUDA(cudaFuncSetAttribute(k_m2l_sparse<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(N_BASE * 32 * sizeof(double2))));
+        KF_CUDA(cudaFuncSetAttribute(k_m2l_sparse<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(N_BASE * 6 * 32 * sizeof(double2))));
       }
+      const int64_t per_cta = (int64_t)SP_WARPS * 16;
+      const dim3 grid((unsigned)std::max<int64_t>(1, (ch.npar + per_cta - 1) / per_cta), (unsigned)Pl.NFG);
       if (Pl.kml == 1)
-        k_m2l_pairsf<1><<<grid, PF_THREADS, smem, Pl.stream>>>(ch.nt, ch.nq, ntb, (int)Pl.NF, Pl.d_that, Pl.d_ub,
-                                                               Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
+        k_m2l_sparse<1><<<grid, SP_WARPS * 32, smem, Pl.stream>>>(ch.npar, ch.nq, Pl.NFP, Pl.d_tbase, Pl.d_rslot,
+                                                                  Pl.d_ub, Pl.d_cb, ch.d_nbr, ch.d_tpat, ch.d_qpat);
       else
-        k_m2l_pairsf<3><<<grid, PF_THREADS, smem, Pl.stream>>>(ch.nt, ch.nq, ntb, (int)Pl.NF, Pl.d_that, Pl.d_ub,
-                                                               Pl.d_cb, ch.d_tpb_pair, ch.d_pl_off, ch.d_pl);
+        k_m2l_sparse<3><<<grid, SP_WARPS * 32, smem, Pl.stream>>>(ch.npar, ch.nq, Pl.NFP, Pl.d_tbase, Pl.d_rslot,
+                                                                  Pl.d_ub, Pl.d_cb, ch.d_nbr, ch.d_tpat, ch.d_qpat);
     } else {
       // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
       // (fewer registers, more resident warps) -- a tuning knob measured in profiles/
@@ -702,7 +745,7 @@ void run_m2l_fft(Plan& Pl) {
       const unsigned grid = (unsigned)((int64_t)npb * Pl.NF);
 #define KF_DMMA(KML, NT)                                                                                        \
   k_m2l_dmma<KML, NT><<<grid, DM_WARPS * 32, 0, Pl.stream>>>(ch.npar, ch.nq, npb, Pl.d_that, Pl.d_ub, Pl.d_cb, \
-                                                             ch.d_nbr, Pl.d_aidx)
+                                                             ch.d_nbr, Pl.d_aidx, Pl.d_fpos, Pl.NFP)
       if (Pl.kml == 1) {
         if (half) KF_DMMA(1, NT_L / 2);
         else KF_DMMA(1, NT_L);
@@ -730,6 +773,104 @@ template <class T>
 static void d2h(Plan& P, std::vector<T>& h, const T* d, int64_t n) {
   h.resize(n);
   if (n) KF_CUDA(cudaMemcpy(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost));
+}
+
+// Frequency groups, positions and the reflected-offset tables of the sparse product
+// (k_m2l_sparse).  Orbits of a bin under (fx, fy) -> (+-fx, +-fy) have 4, 2 or 1
+// members; they are packed into 8-slot phases (never straddling one) and the phases
+// into groups of 32 slots.
+static void build_sparse_tables(Plan& P, const int16_t* tab) {
+  cudaStream_t st = P.stream;
+  const int NG = P.NG, NZ = P.NZ, NF = P.NF;
+  auto fid = [&](int fx, int fy, int fz) { return (fx * NG + fy) * NZ + fz; };
+  std::vector<std::vector<int>> orb[3];  // by size 4, 2, 1
+  std::vector<char> seen(NF, 0);
+  for (int fz = 0; fz < NZ; ++fz)
+    for (int fx = 0; fx < NG; ++fx)
+      for (int fy = 0; fy < NG; ++fy) {
+        if (seen[fid(fx, fy, fz)]) continue;
+        const int rx = (NG - fx) % NG, ry = (NG - fy) % NG;
+        std::vector<int> m;
+        for (int f : {fid(fx, fy, fz), fid(rx, fy, fz), fid(fx, ry, fz), fid(rx, ry, fz)})
+          if (!seen[f]) {
+            seen[f] = 1;
+            m.push_back(f);
+          }
+        orb[m.size() == 4 ? 0 : m.size() == 2 ? 1 : 2].push_back(m);
+      }
+  std::vector<int> slots;  // frequency per slot, -1 = padding
+  for (int k = 0; k < 3; ++k)
+    for (const auto& m : orb[k]) {
+      if ((int)(slots.size() % 8) + (int)m.size() > 8) slots.resize((slots.size() + 7) / 8 * 8, -1);
+      slots.insert(slots.end(), m.begin(), m.end());
+    }
+  slots.resize((slots.size() + 31) / 32 * 32, -1);
+  P.NFG = (int)slots.size() / 32;
+  P.NFP = (int)slots.size();
+  std::vector<int16_t> fpos(NF, -1);
+  for (int i = 0; i < P.NFP; ++i)
+    if (slots[i] >= 0) fpos[slots[i]] = (int16_t)i;
+  std::vector<int> rslot(P.NFP);
+  for (int i = 0; i < P.NFP; ++i) {
+    int packed = 0;
+    for (int r = 0; r < 4; ++r) {
+      int j = i;
+      if (slots[i] >= 0) {
+        const int f = slots[i], fz = f % NZ, fy = (f / NZ) % NG, fx = f / (NZ * NG);
+        const int gx = (r & 1) ? (NG - fx) % NG : fx, gy = (r & 2) ? (NG - fy) % NG : fy;
+        j = fpos[fid(gx, gy, fz)];
+        if (j / 32 != i / 32) throw Error{KAFMM_ECUDA, "sparse M2L: orbit split across groups"};
+      }
+      packed |= (j & 31) << (5 * r);
+    }
+    rslot[i] = packed;
+  }
+  // base offsets |o| (lexicographic over {0..3}^3, max >= 2) -> offset ids
+  std::vector<int16_t> boff;
+  int bidx[64];
+  for (int a = 0; a < 64; ++a) {
+    const int ox = a / 16, oy = (a / 4) % 4, oz = a % 4;
+    bidx[a] = -1;
+    if (std::max(ox, std::max(oy, oz)) >= 2) {
+      bidx[a] = (int)boff.size();
+      boff.push_back(tab[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)]);
+    }
+  }
+  if ((int)boff.size() != N_BASE) throw Error{KAFMM_ECUDA, "sparse M2L: base offset count"};
+  std::vector<uint16_t> info(26 * 64, 0xFFFF);
+  for (int dd = 0; dd < 26; ++dd) {
+    const int d = dd < 13 ? dd : dd + 1;
+    const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
+    for (int b = 0; b < 8; ++b)
+      for (int c = 0; c < 8; ++c) {
+        const int ox = 2 * dx + ((c >> 2) & 1) - ((b >> 2) & 1), oy = 2 * dy + ((c >> 1) & 1) - ((b >> 1) & 1),
+                  oz = 2 * dz + (c & 1) - (b & 1);
+        if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) < 2) continue;
+        const int sx = ox < 0, sy = oy < 0, sz = oz < 0;
+        const int ob = bidx[std::abs(ox) * 16 + std::abs(oy) * 4 + std::abs(oz)];
+        const int r = (sx ^ sz) | ((sy ^ sz) << 1);
+        info[dd * 64 + b * 8 + c] =
+            (uint16_t)(ob | (r << 6) | (sz << 8) | ((sx ^ sy) << 9) | ((sx ^ sz) << 10) | ((sy ^ sz) << 11));
+      }
+  }
+  KF_CUDA(cudaMemcpyToSymbolAsync(c_pinfo, info.data(), info.size() * 2, 0, cudaMemcpyHostToDevice, st));
+  P.d_fpos = dalloc<int16_t>(P, NF);
+  P.d_rslot = dalloc<int>(P, P.NFP);
+  KF_CUDA(cudaMemcpyAsync(P.d_fpos, fpos.data(), NF * 2, cudaMemcpyHostToDevice, st));
+  KF_CUDA(cudaMemcpyAsync(P.d_rslot, rslot.data(), P.NFP * 4, cudaMemcpyHostToDevice, st));
+  int32_t* d_gf;
+  int16_t* d_boff;
+  KF_CUDA(cudaMalloc(&d_gf, P.NFP * 4));
+  KF_CUDA(cudaMalloc(&d_boff, N_BASE * 2));
+  KF_CUDA(cudaMemcpyAsync(d_gf, slots.data(), P.NFP * 4, cudaMemcpyHostToDevice, st));
+  KF_CUDA(cudaMemcpyAsync(d_boff, boff.data(), N_BASE * 2, cudaMemcpyHostToDevice, st));
+  const int nc = P.ncomp;
+  P.d_tbase = dalloc<double2>(P, (size_t)P.NFG * N_BASE * nc * 32);
+  k_tbase<<<nblk((int64_t)P.NFG * N_BASE * nc * 32), 256, 0, st>>>(P.NFG, nc, d_gf, d_boff, P.d_that, P.d_tbase);
+  KF_CHECK_LAUNCH();
+  KF_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_gf);
+  cudaFree(d_boff);
 }
 
 void build_fft_m2l(Plan& P, int64_t budget) {
@@ -866,6 +1007,7 @@ void build_fft_m2l(Plan& P, int64_t budget) {
     cudaFree(spec);
     cudaFree(d_offs);
   }
+  build_sparse_tables(P, tab);
   build_fft_chunks(P, budget);
 }
 
@@ -914,10 +1056,10 @@ void build_fft_chunks(Plan& P, int64_t budget) {
       offid[a] = (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) >= 2) ? (int16_t)id++ : (int16_t)-1;
     }
   }
-  const int64_t per_block = (int64_t)R * P.NF * 16;  // one parent block of spectra
+  const int64_t per_block = (int64_t)R * P.NFP * 16;  // one parent block of spectra
   for (FftChunk& c : P.fft_chunks)  // re-planning (kafmm_restrict): release the old lists
     for (void* p : {(void*)c.d_qbox, (void*)c.d_nbr, (void*)c.d_tbox, (void*)c.d_tpb, (void*)c.d_toff,
-                    (void*)c.d_tpb_pair, (void*)c.d_pl_off, (void*)c.d_pl})
+                    (void*)c.d_tpat, (void*)c.d_qpat})
       dfree(P, p);
   P.fft_chunks.clear();
   P.fft_max_nq = P.fft_max_npar = 0;
@@ -971,41 +1113,58 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         toff.push_back((int32_t)tb.size());
       }
       ch.nt = (int64_t)tb.size();
-      // per-pair product lists in the chunk's target order (Morton; measured better than
-      // grouping targets by octant and sorting lists by offset, which lost the locality
-      // of the source spectra reads: C5 product 1340 -> 1858 ms)
-      std::vector<int2> tpb_pair(tpb);
-      std::vector<int64_t> ploff(1, 0);
-      std::vector<int32_t> pl;
+      // child occupancy of the chunk's target and source parents (sparse product), and a
+      // check that it reproduces the V lists exactly: every V source of a target is a child
+      // of one of the chunk's source parents, and the per-target count equals the existing,
+      // non-adjacent children of its parent's non-leaf colleagues
+      std::vector<uint8_t> tpat(ch.npar, 0), qpat(ch.nq, 0);
+      for (int64_t q = 0; q < ch.npar; ++q)
+        for (int o = 0; o < 8; ++o) {
+          const int32_t c = child[8 * parents[i0 + q] + o];
+          if (c >= 0 && (P.box_active.empty() || P.box_active[c])) tpat[q] |= (uint8_t)(1u << o);
+        }
+      for (int64_t q = 0; q < ch.nq; ++q)
+        for (int o = 0; o < 8; ++o)
+          if (child[8 * (int64_t)qs[q] + o] >= 0) qpat[q] |= (uint8_t)(1u << o);
       for (size_t ii = 0; ii < tb.size(); ++ii) {
         const int32_t t = tb[ii];
         for (int64_t e = voff[t]; e < voff[t + 1]; ++e) {
           const int32_t sb = vsrc[e];
           const int32_t q = qlocal[parent[sb]];
-          const int c = 4 * (ijk[3 * sb] & 1) + 2 * (ijk[3 * sb + 1] & 1) + (ijk[3 * sb + 2] & 1);
           const int ox = ijk[3 * sb] - ijk[3 * t], oy = ijk[3 * sb + 1] - ijk[3 * t + 1],
                     oz = ijk[3 * sb + 2] - ijk[3 * t + 2];
           const int oid = offid[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)];
           if (q < 0 || oid < 0) throw Error{KAFMM_ECUDA, "FFT M2L: V source outside the chunk's parent blocks"};
-          pl.push_back((int32_t)((q * 8 + c) << 9 | oid));
           ++ch.npairs;
         }
-        while (pl.size() % 4) pl.push_back(-1);  // 16-B aligned batches of 4 (one vector load per batch)
-        ploff.push_back((int64_t)pl.size());
+        const int64_t Pq = tpb[ii].x;
+        const int b = tpb[ii].y;
+        int64_t derived = 0;
+        for (int dd = 0; dd < 26; ++dd) {
+          const int32_t q = nb[Pq * 26 + dd];
+          if (q < 0) continue;
+          const int d = dd < 13 ? dd : dd + 1;
+          for (int c = 0; c < 8; ++c) {
+            if (!((qpat[q] >> c) & 1)) continue;
+            const int ox = 2 * (d / 9 - 1) + ((c >> 2) & 1) - ((b >> 2) & 1);
+            const int oy = 2 * ((d / 3) % 3 - 1) + ((c >> 1) & 1) - ((b >> 1) & 1);
+            const int oz = 2 * (d % 3 - 1) + (c & 1) - (b & 1);
+            derived += std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) >= 2;
+          }
+        }
+        if (derived != voff[t + 1] - voff[t])
+          throw Error{KAFMM_ECUDA, "FFT M2L: child occupancy does not reproduce a V list"};
       }
-      if ((int64_t)qs.size() * 8 >= (1 << 22)) throw Error{KAFMM_EINVAL, "FFT M2L chunk too large for pair indices"};
+      if ((int64_t)qs.size() * 8 >= (1 << 22)) throw Error{KAFMM_EINVAL, "FFT M2L chunk too large"};
       {
         int64_t blocks = 0;
         for (int32_t v : nb) blocks += v >= 0;
         ch.block_fill = blocks ? (double)ch.npairs / (64.0 * (double)blocks) : 1.0;
       }
-      ch.d_tpb_pair = dalloc<int2>(P, std::max<size_t>(1, tpb_pair.size()));
-      if (!tpb_pair.empty())
-        KF_CUDA(cudaMemcpyAsync(ch.d_tpb_pair, tpb_pair.data(), tpb_pair.size() * 8, cudaMemcpyHostToDevice, st));
-      ch.d_pl_off = dalloc<int64_t>(P, ploff.size());
-      ch.d_pl = dalloc<int32_t>(P, std::max<size_t>(1, pl.size()));
-      KF_CUDA(cudaMemcpyAsync(ch.d_pl_off, ploff.data(), ploff.size() * 8, cudaMemcpyHostToDevice, st));
-      if (!pl.empty()) KF_CUDA(cudaMemcpyAsync(ch.d_pl, pl.data(), pl.size() * 4, cudaMemcpyHostToDevice, st));
+      ch.d_tpat = dalloc<uint8_t>(P, std::max<int64_t>(1, ch.npar));
+      ch.d_qpat = dalloc<uint8_t>(P, std::max<int64_t>(1, ch.nq));
+      KF_CUDA(cudaMemcpyAsync(ch.d_tpat, tpat.data(), ch.npar, cudaMemcpyHostToDevice, st));
+      if (ch.nq) KF_CUDA(cudaMemcpyAsync(ch.d_qpat, qpat.data(), ch.nq, cudaMemcpyHostToDevice, st));
       ch.d_qbox = dalloc<int32_t>(P, std::max<int64_t>(1, ch.nq));
       ch.d_nbr = dalloc<int32_t>(P, ch.npar * 26);
       ch.d_tbox = dalloc<int32_t>(P, std::max<int64_t>(1, ch.nt));
@@ -1028,8 +1187,8 @@ void build_fft_chunks(Plan& P, int64_t budget) {
   }
   dfree(P, P.d_ub);
   dfree(P, P.d_cb);
-  P.d_ub = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_nq) * R * ((P.NF + PFB - 1) / PFB * PFB));
-  P.d_cb = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_npar) * R * P.NF);
+  P.d_ub = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_nq) * R * P.NFP);
+  P.d_cb = dalloc<double2>(P, (size_t)std::max<int64_t>(1, P.fft_max_npar) * R * P.NFP);
 }
 
 }  // namespace kafmm

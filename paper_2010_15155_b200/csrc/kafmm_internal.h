@@ -71,12 +71,12 @@ struct FftChunk {
   int32_t* d_tbox = nullptr;  // nt target box ids
   int2* d_tpb = nullptr;      // nt: (local parent index, child octant)
   int32_t* d_toff = nullptr;  // npar + 1: targets of local parent P are [toff[P], toff[P+1])
-  // the same V pairs as a per-target list (for sparse chunks): entry
-  // (q * 8 + c) << 9 | offset id, source = child c of source parent q
-  int64_t npairs = 0;
-  int2* d_tpb_pair = nullptr;   // nt: (parent, octant) of the pair lists' target order
-  int64_t* d_pl_off = nullptr;  // nt + 1
-  int32_t* d_pl = nullptr;      // npairs
+  // child occupancy for the sparse-chunk product (k_m2l_sparse): bit c of tpat[P] =
+  // target parent P's child c exists (and is active on this rank); qpat[q] the same
+  // for source parent q's children
+  int64_t npairs = 0;           // V pairs of the chunk
+  uint8_t* d_tpat = nullptr;    // npar
+  uint8_t* d_qpat = nullptr;    // nq
   double block_fill = 1.0;      // V pairs / (8x8 child blocks the DMMA product runs)
 };
 
@@ -197,6 +197,13 @@ struct Plan {
   // FFT M2L (convolution on the NG^3 lattice grid, NG = 2p - 1)
   int m2l_mode = M2L_FFT;
   int NG = 0, NZ = 0, NF = 0;      // grid, half-spectrum NG/2+1, bins NG*NG*NZ
+  // frequency groups of the sparse-chunk product: NFG groups of 32 slots, each a union
+  // of whole orbits {(+-fx, +-fy, fz)}; spectra rows are stored in group-slot order
+  // (position fpos[f] = 32 g + slot), NFP = 32 NFG >= NF positions per row
+  int NFG = 0, NFP = 0;
+  int16_t* d_fpos = nullptr;       // [NF] position of frequency f
+  int* d_rslot = nullptr;          // [NFG][32] slots of R f, R in {id, x, y, xy reflections}, 4 x 5 bits
+  double2* d_tbase = nullptr;      // [NFG][56][ncomp][32] spectra of the 56 offsets with o >= 0
   int ncomp = 0;                   // stored components per operator spectrum: 1 (L) or 6 (sym. G)
   double2* d_that = nullptr;       // [NF][316][ncomp] operator spectra at level 0
   int16_t* d_lat = nullptr;        // M x 3 integer lattice coordinates of the surface points
@@ -204,8 +211,8 @@ struct Plan {
   int16_t* d_aidx = nullptr;       // DMMA A-fragment gather table [26][8kml/4][kml][32]
   double *d_wz = nullptr, *d_wf = nullptr, *d_wi = nullptr;  // DFT-pass twiddle fragments
   std::vector<FftChunk> fft_chunks;
-  double2* d_ub = nullptr;         // [NF][nq][8 kml] source spectra by parent block
-  double2* d_cb = nullptr;         // [npar][8 kml][NF] target check spectra, target-major (contiguous per target)
+  double2* d_ub = nullptr;         // source spectra: dense chunks [NF][nq][8 kml], sparse chunks [NFG][nq][8 kml][32]
+  double2* d_cb = nullptr;         // [npar][8 kml][NFP] target check spectra, target-major, group-slot order
   int64_t fft_max_nq = 0, fft_max_npar = 0, fft_budget = 0;
 
   Jobs J;
@@ -311,7 +318,8 @@ void pack_ue(Plan& P, const int32_t* ids, int64_t n, double* buf);
 void unpack_ue(Plan& P, const int32_t* ids, int64_t n, const double* buf);
 void gather_rows(Plan& P, const double* src, int ld, const int64_t* idx, int64_t n, double* dst);
 void scatter_rows(Plan& P, const double* src, int ld, const int64_t* idx, int64_t n, double* dst);
-void check_values(Plan& P, const double* d_src);             // kafmm_eval.cu
+void check_values(Plan& P, const double* d_src);
+void take_nonfinite(Plan& P);             // kafmm_eval.cu
 void launch_gemm(Plan& P, const GemmBatch& g, const double* A, int M, int K, int lda,
                  const double* B, int ldb, double* C, int ldc, int mode);  // kafmm_gemm.cu
 void build_fft_m2l(Plan& P, int64_t budget_bytes);           // kafmm_fft.cu

@@ -78,6 +78,21 @@ def test_invalid_inputs_fail_loudly():
     v[3, 3] = -1.0
     with pytest.raises(KafmmError):
         plan.check_values(v)
+    # the evaluation itself flags bad values without a host sync; kafmm_sync and
+    # kafmm_eval_host report KAFMM_ENONFINITE once, then the flag is clear
+    plan.eval(v)
+    with pytest.raises(KafmmError) as e:
+        plan.sync()
+    assert e.value.status == 3
+    plan.sync()
+    good = WL.random_values("rpy", 100, 9)
+    bad_v = good.copy()
+    bad_v[7, 1] = np.inf
+    with pytest.raises(KafmmError) as e:
+        plan.eval_host(bad_v)
+    assert e.value.status == 3
+    plan.eval_host(good)
+    plan.sync()
 
 
 def test_superposition_and_scale_covariance_at_size():
