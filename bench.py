@@ -266,23 +266,23 @@ def main():
     else:
         # N GPUs: ONE problem split by Morton ranges (strong scaling); every rank
         # holds a contiguous slice of the user rows and gets its rows' outputs back
-        from paper_2010_15155_b200.dist import DistKAFMM
+        from paper_2010_15155_b200.dist import dist_plan
         offs = np.linspace(0, spec.n, world + 1).astype(np.int64)
         lo, hi = int(offs[rank]), int(offs[rank + 1])
         torch.cuda.synchronize()
         t_setup = time.perf_counter()
-        dk = DistKAFMM(spec_pts[lo:hi], spec.kernel, spec.p, spec.cap, stream=stream)
+        plan = dist_plan(spec_pts[lo:hi], spec.kernel, spec.p, spec.cap, stream=stream)
         torch.cuda.synchronize()
         t_setup = time.perf_counter() - t_setup
-        plan = dk.ctx.plan
         info = plan.info()
+        dinfo = plan.dist_info()
         h_vals = np.ascontiguousarray(vals[lo:hi])
         src = torch.from_numpy(h_vals).cuda()
-        run_step = lambda: dk.eval(src)  # noqa: E731
-        n_v_local, n_p2p_local = dk.ctx.work["n_v"], dk.ctx.work["n_p2p"]
+        out = torch.empty((hi - lo, info.k_t), dtype=torch.float64, device="cuda")
+        run_step = lambda: plan.eval(src, out)  # noqa: E731
+        n_v_local, n_p2p_local = dinfo["n_v_local"], dinfo["n_p2p_local"]
         def run_e2e(hsrc, hout):
-            o = dk.eval(torch.from_numpy(hsrc).cuda(non_blocking=True))
-            torch.from_numpy(hout).copy_(o)  # straight into the pinned host buffer
+            plan.eval_host(hsrc, hout)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
@@ -389,7 +389,8 @@ def main():
                 f"{n_v_local} V pairs = {m2l_flop:.3e} flop")
         kname = ("m2l product: k_m2l_dmma (dense chunks: per-frequency complex GEMM over parent blocks, "
                  "DMMA.8x8x4, 3 real products per complex multiply-add = 6 of the 8 algorithmic flops) + "
-                 "k_m2l_pairsf (sparse chunks: per V pair on the DFMA pipe)")
+                 "k_m2l_sparse (sparse chunks: warp per target parent over 32 bins, absent child pairs skipped, "
+                 "on the DFMA pipe)")
     else:
         m2l_flop = 2.0 * n * n * n_v_local
         algo = f"dense M2L: 2 n^2 flop per V pair, n={n}, {n_v_local} pairs = {m2l_flop:.3e} flop"
@@ -451,6 +452,10 @@ def main():
         "setup": {"s": t_setup, "plan_bytes": int(info.workspace_bytes), "n_boxes": int(info.n_boxes),
                   "note": "kafmm_setup (tree, lists, operators, FFT tables) wall clock, rank 0; not part of value"},
     }
+    if use_dist:
+        line["dist"] = {k: (v.tolist() if hasattr(v, "tolist") else v) for k, v in dinfo.items()}
+        line["dist"]["note"] = ("rank 0's partition: kafmm_setup_dist (NCCL inside libkafmm); plan_bytes is this "
+                                "rank's device memory, bytes_per_eval what it sends per evaluation")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = {k: v for k, v in oracle_sample_rate(spec, spec_pts, vals, args.cpu_budget,
                                                                     args.sample_points).items()

@@ -42,7 +42,7 @@ typedef enum {
   KAFMM_ENONFINITE = 3, /* NaN/Inf in points or values, or negative b / eps */
   KAFMM_ENOMEM = 4,     /* device allocation failed */
   KAFMM_ECUDA = 5,      /* CUDA / cuBLAS / cuSOLVER error (detail in kafmm_last_error) */
-  KAFMM_ENCCL = 6,      /* reserved: multi-GPU exchange error */
+  KAFMM_ENCCL = 6,      /* NCCL error, or libnccl.so.2 missing (multi-GPU plans) */
   KAFMM_ESTATE = 7      /* invalid plan state */
 } kafmm_status;
 
@@ -222,36 +222,57 @@ kafmm_status kafmm_launch_count(kafmm_plan plan, int* n);
  * 1 DFMA loop, over 4 CTAs of 256 threads per SM.  Result in TFLOP/s. */
 kafmm_status kafmm_fp64_peak(int which, double* tflops);
 
-/* ---- multi-GPU building blocks (paper_2010_15155_b200/dist.py) ----
- * One process per GPU.  Every rank builds the plan of the GLOBAL point set
- * with kafmm_setup and then restricts it to a contiguous range of the
- * Morton-sorted points (whole leaves), [plo, phi) in the order of
- * kafmm_get_permutation.  The restricted plan's evaluation is split in two
- * so the caller can exchange multipoles between the passes:
- *   kafmm_eval_up    a1-a4 over the owned leaves (S2M, UC2UE) and M2M into
- *                    every box whose subtree holds owned points; boxes that
- *                    straddle ranks hold this rank's partial sum
- *   (caller)         all-reduce the straddling boxes' UE, receive the ghost
- *                    UE of remote boxes this rank's V/W lists name
- *   kafmm_eval_down  a5-a12 for the active boxes and owned leaves; writes the
- *                    rows of trg_out (user order) of the owned points only
- * src_values of kafmm_eval_up is a full n x k_s user-order array of which the
- * rows of owned points and of the remote U/X-list leaves must be valid.
- * EINVAL if [plo, phi) is outside [0, n) or cuts a leaf; ESTATE if already
- * restricted.  kafmm_eval on a restricted plan runs both passes back to back. */
-kafmm_status kafmm_restrict(kafmm_plan plan, int64_t plo, int64_t phi);
-kafmm_status kafmm_eval_up(kafmm_plan plan, const double* src_values);
-kafmm_status kafmm_eval_down(kafmm_plan plan, double* trg_out);
-/* UE rows of boxes ids[0..n) (device int32) <-> buf (device, n x n_equiv,
- * row-major), on the plan's stream. */
-kafmm_status kafmm_pack_ue(kafmm_plan plan, const int32_t* ids, int64_t n, double* buf);
-kafmm_status kafmm_unpack_ue(kafmm_plan plan, const int32_t* ids, int64_t n, const double* buf);
-/* Row movers on the plan's stream (device pointers, rows of ld doubles):
- * gather dst[j] = src[idx[j]], scatter dst[idx[j]] = src[j], j < n. */
-kafmm_status kafmm_gather_rows(kafmm_plan plan, const double* src, int ld, const int64_t* idx, int64_t n,
-                               double* dst);
-kafmm_status kafmm_scatter_rows(kafmm_plan plan, const double* src, int ld, const int64_t* idx, int64_t n,
-                                double* dst);
+/* ---- multi-GPU (the paper's MPI domain decomposition,
+ * PAPER.md:600-603 and App. D :918-933) ---------------------------------------
+ * One process per GPU.  Each rank passes its own rows of the point set; the
+ * global point set is the concatenation of the ranks' rows in rank order.
+ * Setup all-gathers the points, builds the global octree and lists on every
+ * rank (the same deterministic build), cuts the Morton-sorted points into
+ * contiguous ranges of whole leaves balancing an estimate of the work, and
+ * keeps on each rank only what its range needs: per-box equivalent / check
+ * rows for the boxes whose subtree holds its points, the boxes straddling
+ * ranks and the remote boxes its V / W lists name (ghosts); source records for
+ * its points and the points of remote U / X leaves.
+ * kafmm_eval (and kafmm_eval_host) on such a plan take this caller's n_local
+ * rows of source values and return its n_local rows of outputs; inside, the
+ * plan exchanges source values, straddling-box partial multipoles (all-reduce),
+ * ghost multipoles and outputs over NCCL on the plan's stream, with the near
+ * field (P2P) overlapping the multipole exchanges.  Every rank must call
+ * kafmm_eval the same number of times (collective).  Results equal the
+ * single-GPU plan's to rounding.
+ *
+ * kafmm_get_unique_id: a new NCCL unique id (rank 0; the caller broadcasts the
+ *   128 bytes, e.g. with torch.distributed).  ENCCL if libnccl.so.2 cannot be
+ *   opened (it is loaded at run time; a process that imported torch uses
+ *   torch's copy).
+ * kafmm_setup_dist: collective over `world` ranks; local_points device n_local x 3
+ *   in [0,1)^3 (n_local may be 0; the total must be >= 1).  The plan owns its
+ *   NCCL communicator.  ENCCL on a communicator failure. */
+kafmm_status kafmm_get_unique_id(unsigned char id[128]);
+kafmm_status kafmm_setup_dist(const double* local_points, int64_t n_local, int kernel, int p, int max_pts_per_leaf,
+                              int rank, int world, const unsigned char id[128], kafmm_plan* out);
+
+/* In-process test transport: `world` communicators whose ranks are host
+ * threads of this process sharing one GPU (a host barrier plus device copies;
+ * the ranks' kernels never wait on each other).  comms[world] receives the
+ * handles; each is borrowed by one kafmm_setup_dist_comm call from its own
+ * thread and must outlive that plan; free with kafmm_comm_destroy. */
+typedef struct kafmm_comm_s* kafmm_comm;
+kafmm_status kafmm_comm_local_create(int world, kafmm_comm* comms);
+void kafmm_comm_destroy(kafmm_comm comm);
+kafmm_status kafmm_setup_dist_comm(const double* local_points, int64_t n_local, int kernel, int p,
+                                   int max_pts_per_leaf, kafmm_comm comm, kafmm_plan* out);
+
+/* Partition facts of a kafmm_setup_dist plan (ESTATE for a single-GPU plan):
+ *   what = 0: out[14] = rank, world, global points, caller rows, owned points,
+ *             local points (owned + ghost), ghost points, heavy rows, ghost
+ *             boxes, straddling boxes, plan device bytes, bytes this rank sends
+ *             per eval (values, ghost UE, outputs, all-reduce), V pairs with a
+ *             target on this rank, P2P pairs of its leaves
+ *   what = 1: out[world + 1] = Morton cuts (rank r owns sorted points [c_r, c_r+1))
+ *   what = 2: out[6 world] = rows per peer: values sent, values received, ghost
+ *             UE sent, ghost UE received, outputs sent, outputs received */
+kafmm_status kafmm_dist_query(kafmm_plan plan, int what, int64_t* out);
 
 /* ---- RPY above a no-slip wall (Table X) ----
  * Particles in [0,1) x [0,1) x (1/2, 1) above the wall plane z = 1/2 (device,

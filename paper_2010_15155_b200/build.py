@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkafmm.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["kafmm_tree.cu", "kafmm_ops.cu", "kafmm_gemm.cu", "kafmm_eval.cu", "kafmm_capi.cu", "kafmm_peak.cu", "kafmm_fft.cu", "kafmm_dist.cu", "kafmm_wall.cu"]
+SOURCES = ["kafmm_tree.cu", "kafmm_ops.cu", "kafmm_gemm.cu", "kafmm_eval.cu", "kafmm_capi.cu", "kafmm_peak.cu", "kafmm_fft.cu", "kafmm_dist.cu", "kafmm_comm.cu", "kafmm_wall.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-DKAFMM_BUILD"]
 
@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(one, SOURCES))
     tmp = LIB + ".tmp"
-    cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-lcublas", "-lcusolver", "-lcufft", "-lcudart"]
+    cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-lcublas", "-lcusolver", "-lcufft", "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -43,6 +43,7 @@ static void free_plan(kafmm_plan_s* P) {
   if (P->ev_gout) cudaEventDestroy(P->ev_gout);
   if (P->ev_near_in) cudaEventDestroy(P->ev_near_in);
   if (P->ev_near_out) cudaEventDestroy(P->ev_near_out);
+  delete P->dist;
   delete P;
 }
 }  // namespace kafmm
@@ -82,6 +83,65 @@ static void collect_stage_times(Plan& P) {
     return KAFMM_ECUDA;                            \
   }
 
+namespace kafmm {
+// problem constants of a plan (no device work)
+static void init_plan(Plan& P, int kernel, int p, int cap, int64_t n, int ks, int kt) {
+  P.kernel = kernel;
+  P.p = p;
+  P.cap = cap;
+  P.n = n;
+  P.ks = ks;
+  P.kt = kt;
+  const bool laplace =
+      kernel == KAFMM_LAPLACE_PGRAD || kernel == KAFMM_LAPLACE_PGRADGRAD || kernel == KAFMM_LAPLACE_QPGRADGRAD;
+  P.kml = laplace ? 1 : 3;
+  P.srec = (3 + ks + 3) / 4 * 4;  // x, y, z + source values, padded to 32 bytes
+  P.M = 6 * (p - 1) * (p - 1) + 2;
+  P.neq = P.kml * P.M;
+  P.ldn = round_up(P.neq, GEMM_BK);
+  P.stream = 0;
+}
+
+// tree, lists, operators, GEMM batches, FFT M2L tables and chunks
+void build_plan_core(Plan& P, const double* points) {
+  build_tree_and_lists(P, points);
+  build_operators(P);
+  build_gemm_batches(P);
+  size_t fr = 0, tot = 0;
+  KF_CUDA(cudaMemGetInfo(&fr, &tot));
+  // spectra budget of the FFT M2L chunks: larger chunks transform fewer halo boxes twice
+  int64_t budget = std::min<int64_t>((int64_t)40 << 30, (int64_t)(fr / 3));
+  const char* env = getenv("KAFMM_FFT_BUDGET_MB");
+  if (env) budget = (int64_t)atoll(env) << 20;
+  build_fft_m2l(P, budget);
+  const char* m = getenv("KAFMM_M2L");
+  if (m && std::string(m) == "dense") P.m2l_mode = M2L_DENSE;
+  if (P.m2l_mode == M2L_DENSE) build_dense_m2l(P);
+  P.nrow = P.nbox;
+  P.d_crow = P.d_child;
+  P.nloc = P.n;
+  P.d_operm = P.d_perm;
+}
+
+// per-evaluation workspaces (sized by rows and local points), streams, events
+void alloc_workspaces(Plan& P) {
+  P.d_rec = dalloc<double>(P, (size_t)P.nloc * P.srec);
+  P.d_outs = dalloc<double>(P, (size_t)P.nloc * P.kt);
+  P.d_ue = dalloc<double>(P, (size_t)P.nrow * P.ldn);
+  P.d_chk = dalloc<double>(P, (size_t)P.nrow * P.ldn);
+  P.d_de = dalloc<double>(P, (size_t)P.nrow * P.ldn);
+  P.d_t = dalloc<double>(P, (size_t)P.nrow * P.ldk);
+  for (auto& e : P.ev) KF_CUDA(cudaEventCreate(&e));
+  KF_CUDA(cudaStreamCreateWithFlags(&P.side, cudaStreamNonBlocking));
+  KF_CUDA(cudaStreamCreateWithFlags(&P.gstream, cudaStreamNonBlocking));
+  KF_CUDA(cudaEventCreateWithFlags(&P.ev_gin, cudaEventDisableTiming));
+  KF_CUDA(cudaEventCreateWithFlags(&P.ev_gout, cudaEventDisableTiming));
+  KF_CUDA(cudaEventCreateWithFlags(&P.ev_near_in, cudaEventDisableTiming));
+  KF_CUDA(cudaEventCreateWithFlags(&P.ev_near_out, cudaEventDisableTiming));
+  KF_CUDA(cudaStreamSynchronize(P.stream));
+}
+}  // namespace kafmm
+
 extern "C" {
 
 kafmm_status kafmm_kernel_dims(int kernel, int* k_s, int* k_t) {
@@ -95,66 +155,36 @@ kafmm_status kafmm_kernel_dims(int kernel, int* k_s, int* k_t) {
   return KAFMM_OK;
 }
 
+
+static kafmm_status check_setup_args(int64_t n, int kernel, int p, int max_pts, int* ks, int* kt, const char* who) {
+  if (n < 1 || n > INT32_MAX || p < 2 || max_pts < 1 || dims(kernel, ks, kt) != 0) {
+    set_error(std::string(who) + ": invalid argument");
+    return KAFMM_EINVAL;
+  }
+  if (6 * (p - 1) * (p - 1) + 2 > KAFMM_MAX_SURFACE) {  // the leaf kernels stage one surface per CTA
+    set_error(std::string(who) + ": p too large (surface of 6(p-1)^2+2 points exceeds 1024; p <= 14)");
+    return KAFMM_EINVAL;
+  }
+  return KAFMM_OK;
+}
+
 kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int max_pts_per_leaf,
                          kafmm_plan* out) {
   if (out) *out = nullptr;
   int ks, kt;
-  if (!points || !out || n < 1 || n > INT32_MAX || p < 2 || max_pts_per_leaf < 1 || dims(kernel, &ks, &kt) != 0) {
+  if (!points || !out) {
     set_error("kafmm_setup: invalid argument");
     return KAFMM_EINVAL;
   }
-  if (6 * (p - 1) * (p - 1) + 2 > KAFMM_MAX_SURFACE) {  // the leaf kernels stage one surface per CTA
-    set_error("kafmm_setup: p too large (surface of 6(p-1)^2+2 points exceeds 1024; p <= 14)");
-    return KAFMM_EINVAL;
-  }
+  if (kafmm_status st = check_setup_args(n, kernel, p, max_pts_per_leaf, &ks, &kt, "kafmm_setup")) return st;
   kafmm_plan_s* P = nullptr;
   KF_API_BEGIN
   int dev = 0;
   KF_CUDA(cudaGetDevice(&dev));
   P = new kafmm_plan_s();
-  P->kernel = kernel;
-  P->p = p;
-  P->cap = max_pts_per_leaf;
-  P->n = n;
-  P->ks = ks;
-  P->kt = kt;
-  const bool laplace =
-      kernel == KAFMM_LAPLACE_PGRAD || kernel == KAFMM_LAPLACE_PGRADGRAD || kernel == KAFMM_LAPLACE_QPGRADGRAD;
-  P->kml = laplace ? 1 : 3;
-  P->srec = (3 + ks + 3) / 4 * 4;  // x, y, z + source values, padded to 32 bytes
-  P->M = 6 * (p - 1) * (p - 1) + 2;
-  P->neq = P->kml * P->M;
-  P->ldn = round_up(P->neq, GEMM_BK);
-  P->stream = 0;
-  build_tree_and_lists(*P, points);
-  build_operators(*P);
-  build_gemm_batches(*P);
-  {
-    size_t fr = 0, tot = 0;
-    KF_CUDA(cudaMemGetInfo(&fr, &tot));
-    // spectra budget of the FFT M2L chunks: larger chunks transform fewer halo boxes twice
-    int64_t budget = std::min<int64_t>((int64_t)40 << 30, (int64_t)(fr / 3));
-    const char* env = getenv("KAFMM_FFT_BUDGET_MB");
-    if (env) budget = (int64_t)atoll(env) << 20;
-    build_fft_m2l(*P, budget);
-    const char* m = getenv("KAFMM_M2L");
-    if (m && std::string(m) == "dense") P->m2l_mode = M2L_DENSE;
-    if (P->m2l_mode == M2L_DENSE) build_dense_m2l(*P);
-  }
-  P->d_rec = dalloc<double>(*P, (size_t)n * P->srec);
-  P->d_outs = dalloc<double>(*P, (size_t)n * kt);
-  P->d_ue = dalloc<double>(*P, (size_t)P->nbox * P->ldn);
-  P->d_chk = dalloc<double>(*P, (size_t)P->nbox * P->ldn);
-  P->d_de = dalloc<double>(*P, (size_t)P->nbox * P->ldn);
-  P->d_t = dalloc<double>(*P, (size_t)P->nbox * P->ldk);
-  for (auto& e : P->ev) KF_CUDA(cudaEventCreate(&e));
-  KF_CUDA(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
-  KF_CUDA(cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking));
-  KF_CUDA(cudaEventCreateWithFlags(&P->ev_gin, cudaEventDisableTiming));
-  KF_CUDA(cudaEventCreateWithFlags(&P->ev_gout, cudaEventDisableTiming));
-  KF_CUDA(cudaEventCreateWithFlags(&P->ev_near_in, cudaEventDisableTiming));
-  KF_CUDA(cudaEventCreateWithFlags(&P->ev_near_out, cudaEventDisableTiming));
-  KF_CUDA(cudaStreamSynchronize(P->stream));
+  init_plan(*P, kernel, p, max_pts_per_leaf, n, ks, kt);
+  build_plan_core(*P, points);
+  alloc_workspaces(*P);
   *out = P;
   return KAFMM_OK;
   }
@@ -171,6 +201,110 @@ kafmm_status kafmm_setup(const double* points, int64_t n, int kernel, int p, int
   }
 }
 
+// multi-GPU: the plan of this rank's part of a point set spread over the ranks
+static kafmm_status setup_dist_common(const double* local_points, int64_t n_local, int kernel, int p, int max_pts,
+                                      Comm* comm, bool owns, kafmm_plan* out) {
+  if (out) *out = nullptr;
+  int ks, kt;
+  if (!out || n_local < 0 || (n_local > 0 && !local_points) || !comm) {
+    if (owns) delete comm;
+    set_error("kafmm_setup_dist: invalid argument");
+    return KAFMM_EINVAL;
+  }
+  if (kafmm_status st = check_setup_args(1, kernel, p, max_pts, &ks, &kt, "kafmm_setup_dist")) {
+    if (owns) delete comm;
+    return st;
+  }
+  kafmm_plan_s* P = nullptr;
+  KF_API_BEGIN
+  P = new kafmm_plan_s();
+  P->dist = new DistState();
+  P->dist->comm = comm;
+  P->dist->owns_comm = owns;
+  init_plan(*P, kernel, p, max_pts, 0, ks, kt);
+  setup_dist(*P, local_points, n_local);
+  *out = P;
+  return KAFMM_OK;
+  }
+  catch (const Error& e) {
+    set_error(e.msg);
+    if (P) free_plan(P);
+    else if (owns) delete comm;
+    cudaGetLastError();
+    return e.st;
+  }
+  catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    if (P) free_plan(P);
+    else if (owns) delete comm;
+    return KAFMM_ENOMEM;
+  }
+}
+
+kafmm_status kafmm_get_unique_id(unsigned char id[128]) {
+  if (!id) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  nccl_unique_id(id);
+  return KAFMM_OK;
+  KF_API_END
+}
+
+kafmm_status kafmm_setup_dist(const double* local_points, int64_t n_local, int kernel, int p, int max_pts_per_leaf,
+                              int rank, int world, const unsigned char id[128], kafmm_plan* out) {
+  if (out) *out = nullptr;
+  if (!id || world < 1 || rank < 0 || rank >= world) {
+    set_error("kafmm_setup_dist: invalid rank / world / id");
+    return KAFMM_EINVAL;
+  }
+  Comm* c = nullptr;
+  KF_API_BEGIN
+  c = make_nccl_comm(id, rank, world);
+  KF_API_END
+  return setup_dist_common(local_points, n_local, kernel, p, max_pts_per_leaf, c, true, out);
+}
+
+kafmm_status kafmm_comm_local_create(int world, kafmm_comm* comms) {
+  if (world < 1 || !comms) return KAFMM_EINVAL;
+  KF_API_BEGIN
+  std::vector<Comm*> c(world);
+  make_local_comms(world, c.data());
+  for (int r = 0; r < world; ++r) comms[r] = reinterpret_cast<kafmm_comm>(c[r]);
+  return KAFMM_OK;
+  KF_API_END
+}
+
+void kafmm_comm_destroy(kafmm_comm comm) { delete reinterpret_cast<Comm*>(comm); }
+
+kafmm_status kafmm_setup_dist_comm(const double* local_points, int64_t n_local, int kernel, int p,
+                                   int max_pts_per_leaf, kafmm_comm comm, kafmm_plan* out) {
+  return setup_dist_common(local_points, n_local, kernel, p, max_pts_per_leaf, reinterpret_cast<Comm*>(comm), false,
+                           out);
+}
+
+kafmm_status kafmm_dist_query(kafmm_plan plan, int what, int64_t* out) {
+  if (!plan || !out) return KAFMM_EINVAL;
+  const Plan& P = *plan;
+  if (!P.dist) {
+    set_error("kafmm_dist_query: not a partitioned plan");
+    return KAFMM_ESTATE;
+  }
+  const DistState& D = *P.dist;
+  if (what == 0) {
+    const int64_t v[14] = {D.rank, D.world, D.n_global, D.n_caller, D.n_owned, P.nloc, D.n_ghost_points,
+                           P.nrow, D.n_ghost_boxes, D.nshared, P.bytes,
+                           8 * (D.e1.stotal + D.e3.stotal + D.e4.stotal + D.nshared * P.neq), D.n_v_local,
+                           D.n_p2p_local};
+    for (int i = 0; i < 14; ++i) out[i] = v[i];
+  } else if (what == 1) {
+    for (int i = 0; i <= D.world; ++i) out[i] = D.cuts[i];
+  } else if (what == 2) {
+    for (size_t i = 0; i < D.counts.size(); ++i) out[i] = D.counts[i];
+  } else {
+    return KAFMM_EINVAL;
+  }
+  return KAFMM_OK;
+}
+
 kafmm_status kafmm_set_stream(kafmm_plan plan, void* stream) {
   if (!plan) return KAFMM_EINVAL;
   plan->stream = (cudaStream_t)stream;
@@ -184,6 +318,11 @@ kafmm_status kafmm_eval(kafmm_plan plan, const double* src_values, double* trg_o
   }
   KF_API_BEGIN
   Plan& P = *plan;
+  if (P.dist) {  // partitioned plan: this caller's rows in and out, exchanges inside
+    run_eval_dist(P, src_values, trg_out);
+    collect_stage_times(P);
+    return KAFMM_OK;
+  }
   if (P.use_graph && P.timing == 0 && P.graph_warm) {
     if (!P.gexec || P.g_src != src_values || P.g_out != trg_out || P.g_mode != P.m2l_mode) {
       if (P.gexec) KF_CUDA(cudaGraphExecDestroy(P.gexec));
@@ -306,13 +445,15 @@ kafmm_status kafmm_eval_host(kafmm_plan plan, const double* src_values, double* 
   }
   KF_API_BEGIN
   Plan& P = *plan;
+  const int64_t rows = P.dist ? P.dist->n_caller : P.n;  // the caller's rows
   if (!P.d_stage_in) {
-    P.d_stage_in = dalloc<double>(P, (size_t)P.n * P.ks);
-    P.d_stage_out = dalloc<double>(P, (size_t)P.n * P.kt);
+    P.d_stage_in = dalloc<double>(P, (size_t)std::max<int64_t>(1, rows) * P.ks);
+    P.d_stage_out = dalloc<double>(P, (size_t)std::max<int64_t>(1, rows) * P.kt);
   }
-  KF_CUDA(cudaMemcpyAsync(P.d_stage_in, src_values, (size_t)P.n * P.ks * 8, cudaMemcpyHostToDevice, P.stream));
-  run_eval(P, P.d_stage_in, P.d_stage_out);
-  KF_CUDA(cudaMemcpyAsync(trg_out, P.d_stage_out, (size_t)P.n * P.kt * 8, cudaMemcpyDeviceToHost, P.stream));
+  KF_CUDA(cudaMemcpyAsync(P.d_stage_in, src_values, (size_t)rows * P.ks * 8, cudaMemcpyHostToDevice, P.stream));
+  if (P.dist) run_eval_dist(P, P.d_stage_in, P.d_stage_out);
+  else run_eval(P, P.d_stage_in, P.d_stage_out);
+  KF_CUDA(cudaMemcpyAsync(trg_out, P.d_stage_out, (size_t)rows * P.kt * 8, cudaMemcpyDeviceToHost, P.stream));
   KF_CUDA(cudaStreamSynchronize(P.stream));
   take_nonfinite(P);
   return KAFMM_OK;
@@ -402,6 +543,10 @@ kafmm_status kafmm_get_tree(kafmm_plan plan, int32_t* level, int32_t* ijk, int32
 
 kafmm_status kafmm_get_permutation(kafmm_plan plan, int64_t* perm) {
   if (!plan || !perm) return KAFMM_EINVAL;
+  if (plan->dist) {
+    set_error("kafmm_get_permutation: a partitioned plan holds only its local points");
+    return KAFMM_ESTATE;
+  }
   KF_API_BEGIN
   KF_CUDA(cudaMemcpy(perm, plan->d_perm, plan->n * 8, cudaMemcpyDeviceToHost));
   return KAFMM_OK;
@@ -482,71 +627,6 @@ kafmm_status kafmm_get_m2l_mode(kafmm_plan plan, int* mode) {
   if (!plan || !mode) return KAFMM_EINVAL;
   *mode = plan->m2l_mode;
   return KAFMM_OK;
-}
-
-kafmm_status kafmm_restrict(kafmm_plan plan, int64_t plo, int64_t phi) {
-  if (!plan) return KAFMM_EINVAL;
-  KF_API_BEGIN
-  restrict_plan(*plan, plo, phi);
-  return KAFMM_OK;
-  KF_API_END
-}
-
-kafmm_status kafmm_eval_up(kafmm_plan plan, const double* src_values) {
-  if (!plan || !src_values) {
-    set_error("kafmm_eval_up: null argument");
-    return KAFMM_EINVAL;
-  }
-  KF_API_BEGIN
-  run_eval_up(*plan, src_values);
-  return KAFMM_OK;
-  KF_API_END
-}
-
-kafmm_status kafmm_eval_down(kafmm_plan plan, double* trg_out) {
-  if (!plan || !trg_out) {
-    set_error("kafmm_eval_down: null argument");
-    return KAFMM_EINVAL;
-  }
-  KF_API_BEGIN
-  run_eval_down(*plan, trg_out);
-  collect_stage_times(*plan);
-  return KAFMM_OK;
-  KF_API_END
-}
-
-kafmm_status kafmm_pack_ue(kafmm_plan plan, const int32_t* ids, int64_t n, double* buf) {
-  if (!plan || n < 0 || (n > 0 && (!ids || !buf))) return KAFMM_EINVAL;
-  KF_API_BEGIN
-  pack_ue(*plan, ids, n, buf);
-  return KAFMM_OK;
-  KF_API_END
-}
-
-kafmm_status kafmm_unpack_ue(kafmm_plan plan, const int32_t* ids, int64_t n, const double* buf) {
-  if (!plan || n < 0 || (n > 0 && (!ids || !buf))) return KAFMM_EINVAL;
-  KF_API_BEGIN
-  unpack_ue(*plan, ids, n, buf);
-  return KAFMM_OK;
-  KF_API_END
-}
-
-kafmm_status kafmm_gather_rows(kafmm_plan plan, const double* src, int ld, const int64_t* idx, int64_t n,
-                               double* dst) {
-  if (!plan || ld < 1 || n < 0 || (n > 0 && (!src || !idx || !dst))) return KAFMM_EINVAL;
-  KF_API_BEGIN
-  gather_rows(*plan, src, ld, idx, n, dst);
-  return KAFMM_OK;
-  KF_API_END
-}
-
-kafmm_status kafmm_scatter_rows(kafmm_plan plan, const double* src, int ld, const int64_t* idx, int64_t n,
-                                double* dst) {
-  if (!plan || ld < 1 || n < 0 || (n > 0 && (!src || !idx || !dst))) return KAFMM_EINVAL;
-  KF_API_BEGIN
-  scatter_rows(*plan, src, ld, idx, n, dst);
-  return KAFMM_OK;
-  KF_API_END
 }
 
 kafmm_status kafmm_fft_stats(kafmm_plan plan, int64_t* st) {

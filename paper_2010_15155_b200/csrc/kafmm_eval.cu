@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(NTH)
                         const int2* __restrict__ rng, const int32_t* __restrict__ level,
                         const int32_t* __restrict__ ijk, const int64_t* __restrict__ pbeg,
                         const int64_t* __restrict__ pend, const double* __restrict__ rec,
-                        const double* __restrict__ surf, int M, double alpha, double* __restrict__ out, int ldn) {
+                        const double* __restrict__ surf, int M, double alpha, double* __restrict__ out, int ldn,
+                        const int32_t* __restrict__ row) {
   constexpr int CH = STREAM_DOUBLES / SREC;
   __shared__ __align__(16) double ss[CH * SREC];
   const int job = blockIdx.x, tid = threadIdx.x;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(NTH)
     }
   }
   if (fill) run(fill);
-  double* o = out + (int64_t)b * ldn;
+  double* o = out + (int64_t)(row ? row[b] : b) * ldn;
 #pragma unroll
   for (int q = 0; q < TQ; ++q) {
     int i = tid + NTH * q;
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(PT_THREADS)
                const int64_t* __restrict__ pbeg, const int64_t* __restrict__ pend, const double* __restrict__ pts,
                const int64_t* __restrict__ w_off, const int32_t* __restrict__ w_src, const double* __restrict__ ue,
                const double* __restrict__ de, int ldn, const double* __restrict__ surf, int M,
-               double* __restrict__ outs, int add) {
+               double* __restrict__ outs, int add, const int32_t* __restrict__ row) {
   constexpr int CH = STREAM_DOUBLES / SSTR;
   __shared__ __align__(16) double ss[STREAM_DOUBLES];
   const int job = blockIdx.x, tid = threadIdx.x;
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(PT_THREADS)
     for (int64_t e = (lb >= 2 ? e0 - 1 : e0); e < e1; ++e) {
       const bool own = e < e0;
       const int sb = own ? b : w_src[e];
-      const double* dens = (own ? de : ue) + (int64_t)sb * ldn;
+      const double* dens = (own ? de : ue) + (int64_t)(row ? row[sb] : sb) * ldn;
       double cx, cy, cz, h;
       box_geom(level, ijk, sb, cx, cy, cz, h);
       const double sc = (own ? ALPHA_DE : ALPHA_UE) * h;
@@ -379,7 +380,7 @@ static void launch_surface(Plan& P, const int32_t* jobs, int64_t njobs, const in
                            double alpha) {
 #define KF_SURF(TQ, NTH)                                                                                     \
   k_points_to_surface<K, SREC, TQ, ADD, NTH><<<(unsigned)njobs, NTH, 0, P.stream>>>(                       \
-      jobs, roff, rng, P.d_level, P.d_ijk, P.d_pbeg, P.d_pend, P.d_rec, P.d_surf, P.M, alpha, P.d_chk, P.ldn)
+      jobs, roff, rng, P.d_level, P.d_ijk, P.d_pbeg, P.d_pend, P.d_rec, P.d_surf, P.M, alpha, P.d_chk, P.ldn, P.d_row)
   const int M = P.M;
   if (M <= 128) KF_SURF(1, 128);
   else if (M <= 256) KF_SURF(2, 128);
@@ -424,7 +425,7 @@ static void eval_up_impl(Plan& P, const double* d_src) {
   const int sqcol = P.kernel == KAFMM_RPY || P.kernel == KAFMM_STOKES_REG_VEL ? 3
                     : P.kernel == KAFMM_STOKES_REG_VEL_OMEGA        ? 6
                                                                     : -1;
-  k_gather<<<nblk(P.n), 256, 0, st>>>(d_src, P.d_pts, P.d_perm, P.n, P.ks, SREC, sqcol, P.d_rec, P.d_flag + 1);
+  k_gather<<<nblk(P.nloc), 256, 0, st>>>(d_src, P.d_pts, P.d_perm, P.nloc, P.ks, SREC, sqcol, P.d_rec, P.d_flag + 1);
   KF_CHECK_LAUNCH();
   P.launches++;
   // the near field needs only the gathered records: it runs on a side stream
@@ -437,7 +438,7 @@ static void eval_up_impl(Plan& P, const double* d_src) {
     launch_p2p<KST, SREC>(P, P.side, 0);
     KF_CUDA(cudaEventRecord(P.ev_near_out, P.side));
   }
-  KF_CUDA(cudaMemsetAsync(P.d_ue, 0, (size_t)P.nbox * P.ldn * 8, st));
+  KF_CUDA(cudaMemsetAsync(P.d_ue, 0, (size_t)P.nrow * P.ldn * 8, st));
   mark(ST_S2M);
   if (J.ns2m > 0) launch_surface<KS, SREC, false>(P, J.s2m_ids, J.ns2m, nullptr, nullptr, ALPHA_UC);
   mark(ST_UC2UE);
@@ -455,7 +456,7 @@ static void eval_down_impl(Plan& P, double* d_out) {
     if (P.timing == 1 || (P.timing == 2 && (s == ST_GATHER || s == ST_TOTAL))) KF_CUDA(cudaEventRecord(P.ev[s], st));
   };
   const Jobs& J = P.J;
-  KF_CUDA(cudaMemsetAsync(P.d_chk, 0, (size_t)P.nbox * P.ldn * 8, st));
+  KF_CUDA(cudaMemsetAsync(P.d_chk, 0, (size_t)P.nrow * P.ldn * 8, st));
   mark(ST_M2L);
   P.prod_used = 0;
   if (P.m2l_mode != M2L_DENSE) {
@@ -486,7 +487,7 @@ static void eval_down_impl(Plan& P, double* d_out) {
 #define KF_FAR(TP)                                                                                             \
   k_leaf_far<KT_, SST, TP><<<(unsigned)J.nleaf, PT_THREADS, 0, st>>>(J.leaf_ids, P.d_level, P.d_ijk, P.d_pbeg,  \
                                                                     P.d_pend, P.d_pts, J.w_off, J.w_src, P.d_ue, \
-                                                                    P.d_de, P.ldn, P.d_surf, P.M, P.d_outs, far_add)
+                                                                    P.d_de, P.ldn, P.d_surf, P.M, P.d_outs, far_add, P.d_row)
     if (big) KF_FAR(TPT);
     else KF_FAR(1);
 #undef KF_FAR
@@ -499,7 +500,7 @@ static void eval_down_impl(Plan& P, double* d_out) {
   const double scale = (P.kml == 1) ? 1.0 / (4.0 * M_PI) : 1.0 / (8.0 * M_PI);
   const int64_t cnt = (J.phi - J.plo) * P.kt;
   if (cnt > 0) {
-    k_scatter<<<nblk(cnt), 256, 0, st>>>(P.d_outs + J.plo * P.kt, P.d_perm + J.plo, J.phi - J.plo, P.kt, scale,
+    k_scatter<<<nblk(cnt), 256, 0, st>>>(P.d_outs + J.plo * P.kt, P.d_operm + J.plo, J.phi - J.plo, P.kt, scale,
                                          d_out);
     KF_CHECK_LAUNCH();
     P.launches++;
@@ -552,7 +553,8 @@ void check_values(Plan& P, const double* d_src) {
   KF_CUDA(cudaMemsetAsync(P.d_flag, 0, 4, P.stream));
   const int pcol = (P.kernel == KAFMM_RPY || P.kernel == KAFMM_STOKES_REG_VEL) ? 3
                    : (P.kernel == KAFMM_STOKES_REG_VEL_OMEGA ? 6 : -1);
-  k_check_values<<<nblk(P.n * P.ks), 256, 0, P.stream>>>(d_src, P.n, P.ks, pcol, P.d_flag);
+  const int64_t rows = P.dist ? P.dist->n_caller : P.n;  // the caller's rows
+  k_check_values<<<nblk(rows * P.ks), 256, 0, P.stream>>>(d_src, rows, P.ks, pcol, P.d_flag);
   KF_CHECK_LAUNCH();
   int h = 0;
   KF_CUDA(cudaMemcpyAsync(&h, P.d_flag, 4, cudaMemcpyDeviceToHost, P.stream));

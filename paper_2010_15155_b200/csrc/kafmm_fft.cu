@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(256)
 template <int P>
 __global__ void __launch_bounds__(256)
     k_fft_inv(const int32_t* __restrict__ tbox, const int2* __restrict__ tpb, int64_t npar,
-              const int32_t* __restrict__ level, const double2* __restrict__ cb, int kml,
+              int lev, const double2* __restrict__ cb, int kml,
               const int16_t* __restrict__ lat, int M, double* __restrict__ chk, int ldn,
               const double* __restrict__ wi, const int16_t* __restrict__ fpos, int NFP) {
   using D = FftDims<P>;
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256)
   const int64_t box = tbox[t];
   const int2 pb = tpb[t];
   const int R = 8 * kml;
-  const double scale = ldexp(1.0, level[box]) / (double)(NG * NG * NG);
+  const double scale = ldexp(1.0, lev) / (double)(NG * NG * NG);
   for (int j = tid; j < NG; j += bd) {
     double sn, cs;
     sincospi(2.0 * j / NG, &sn, &cs);
@@ -662,7 +662,7 @@ template <int P, int NB>
 static void launch_fwd_nb(Plan& Pl, const FftChunk& ch) {
   const int ng = (8 * Pl.kml + NB - 1) / NB;
   k_fft_fwd<P, NB><<<(unsigned)(ch.nq * ng), 256, FwdCfg<P>::template smem<NB>(), Pl.stream>>>(
-      ch.d_qbox, Pl.d_child, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lmap, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1,
+      ch.d_qbox, Pl.d_crow, ch.nq, Pl.d_ue, Pl.ldn, Pl.kml, Pl.d_lmap, Pl.d_ub, chunk_uses_pairs(Pl, ch) ? 0 : 1,
       Pl.d_wz, Pl.d_wf, Pl.d_fpos);
 }
 
@@ -681,7 +681,7 @@ template <int P>
 static void launch_inv(Plan& Pl, const FftChunk& ch) {
   set_smem_attrs<P>();
   k_fft_inv<P><<<(unsigned)ch.nt, 256, FftDims<P>::INV_SMEM, Pl.stream>>>(
-      ch.d_tbox, ch.d_tpb, ch.npar, Pl.d_level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn, Pl.d_wi,
+      ch.d_tbox, ch.d_tpb, ch.npar, ch.level, Pl.d_cb, Pl.kml, Pl.d_lat, Pl.M, Pl.d_chk, Pl.ldn, Pl.d_wi,
       Pl.d_fpos, Pl.NFP);
   KF_CHECK_LAUNCH();
   Pl.launches++;
@@ -1123,9 +1123,13 @@ void build_fft_chunks(Plan& P, int64_t budget) {
           const int32_t c = child[8 * parents[i0 + q] + o];
           if (c >= 0 && (P.box_active.empty() || P.box_active[c])) tpat[q] |= (uint8_t)(1u << o);
         }
+      // a source child counts if it has a UE row here (every child on one GPU; on a rank,
+      // the active, shared and ghost boxes -- which include every V source of its targets)
       for (int64_t q = 0; q < ch.nq; ++q)
-        for (int o = 0; o < 8; ++o)
-          if (child[8 * (int64_t)qs[q] + o] >= 0) qpat[q] |= (uint8_t)(1u << o);
+        for (int o = 0; o < 8; ++o) {
+          const int32_t c = child[8 * (int64_t)qs[q] + o];
+          if (c >= 0 && (P.h_row.empty() || P.h_row[c] >= 0)) qpat[q] |= (uint8_t)(1u << o);
+        }
       for (size_t ii = 0; ii < tb.size(); ++ii) {
         const int32_t t = tb[ii];
         for (int64_t e = voff[t]; e < voff[t + 1]; ++e) {
@@ -1173,6 +1177,8 @@ void build_fft_chunks(Plan& P, int64_t budget) {
       KF_CUDA(cudaMemcpyAsync(ch.d_toff, toff.data(), toff.size() * 4, cudaMemcpyHostToDevice, st));
       if (ch.nq) KF_CUDA(cudaMemcpyAsync(ch.d_qbox, qs.data(), ch.nq * 4, cudaMemcpyHostToDevice, st));
       KF_CUDA(cudaMemcpyAsync(ch.d_nbr, nb.data(), ch.npar * 26 * 4, cudaMemcpyHostToDevice, st));
+      if (!P.h_row.empty())  // the inverse transform writes CHK rows
+        for (int32_t& t : tb) t = P.h_row[t];
       if (ch.nt) {
         KF_CUDA(cudaMemcpyAsync(ch.d_tbox, tb.data(), ch.nt * 4, cudaMemcpyHostToDevice, st));
         KF_CUDA(cudaMemcpyAsync(ch.d_tpb, tpb.data(), ch.nt * 8, cudaMemcpyHostToDevice, st));

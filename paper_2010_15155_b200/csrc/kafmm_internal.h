@@ -110,6 +110,55 @@ struct Jobs {
   int2* x_rng = nullptr;
 };
 
+// Collectives of the multi-GPU evaluation (kafmm_comm.cu): NCCL, or an
+// in-process group of host threads (test transport).  Counts and
+// displacements are in doubles; every call is ordered on stream s.
+struct Comm {
+  int rank = 0, world = 1;
+  virtual ~Comm() {}
+  virtual void alltoallv(const double* sbuf, const int64_t* sdispl, const int64_t* scount, double* rbuf,
+                         const int64_t* rdispl, const int64_t* rcount, cudaStream_t s) = 0;
+  virtual void allreduce(double* buf, int64_t count, cudaStream_t s) = 0;
+  virtual const char* kind() const = 0;
+  std::vector<int64_t> allgather_count(int64_t mine, cudaStream_t s);
+};
+Comm* make_nccl_comm(const unsigned char id[128], int rank, int world);
+void make_local_comms(int world, Comm** out);
+void nccl_unique_id(unsigned char id[128]);
+
+// One rank's side of the partitioned evaluation (kafmm_dist.cu).  The plan of a
+// rank holds the global tree and lists but heavy per-box rows (UE, CHK, DE, T)
+// only for its active, shared and ghost boxes, and source records only for its
+// owned points and the remote points its U / X lists name.
+struct Exchange {  // one all-to-all-v: counts and displacements in doubles, per peer
+  std::vector<int64_t> scount, sdispl, rcount, rdispl;
+  int64_t stotal = 0, rtotal = 0;
+  double* d_sbuf = nullptr;
+  double* d_rbuf = nullptr;
+};
+struct DistState {
+  Comm* comm = nullptr;
+  bool owns_comm = false;
+  int rank = 0, world = 1;
+  int64_t n_global = 0, n_caller = 0;   // all points; this caller's rows
+  std::vector<int64_t> caller_off;      // world + 1: first global user row of each caller
+  std::vector<int64_t> cuts;            // world + 1: Morton ranges of the ranks
+  Exchange e1, e3, e4;                  // values, ghost UE, outputs
+  int64_t* d_val_idx = nullptr;         // E1 send: caller-local value rows, per destination
+  int64_t* d_out_idx = nullptr;         // E4 receive: caller-local output rows, per source
+  int32_t* d_ue_send_rows = nullptr;    // E3: UE rows packed for the peers
+  int32_t* d_ue_recv_rows = nullptr;    // E3: ghost UE rows unpacked
+  int32_t* d_shared_rows = nullptr;     // E2: rows of the boxes straddling ranks
+  int64_t nshared = 0;
+  double* d_shared_buf = nullptr;
+  int64_t n_ghost_boxes = 0, n_ghost_points = 0, n_owned = 0;
+  int64_t n_v_local = 0, n_p2p_local = 0;  // M2L pairs with an active target, P2P pairs of owned leaves
+  std::vector<int64_t> counts;          // 6 x world: val send/recv, ue send/recv, out send/recv (rows)
+  ~DistState() {
+    if (owns_comm) delete comm;
+  }
+};
+
 enum Stage {
   ST_GATHER = 0, ST_S2M, ST_UC2UE, ST_M2M, ST_M2L, ST_S2L, ST_DC2DE, ST_L2L,
   ST_LEAF_FAR, ST_P2P, ST_SCATTER, ST_TOTAL,
@@ -217,6 +266,15 @@ struct Plan {
 
   Jobs J;
   bool restricted = false;
+  // heavy per-box rows: UE / CHK / DE / T row of box b is d_row[b] (identity for a
+  // single-GPU plan; compacted to active + shared + ghost boxes on a rank)
+  int64_t nrow = 0;
+  int32_t* d_row = nullptr;
+  int32_t* d_crow = nullptr;       // 8 per box: row of the child, or -1 (FFT forward)
+  std::vector<int32_t> h_row;      // host copy (empty: identity)
+  int64_t nloc = 0;                // points with source records (n, or owned + ghost on a rank)
+  int64_t* d_operm = nullptr;      // scatter_out: Morton position -> output row (d_perm unless partitioned)
+  DistState* dist = nullptr;
   // kafmm_setup2: rows [0, n_src) of the union are sources, the rest targets
   int64_t n_src = -1;
   double* d_uvals = nullptr;   // union source values (target rows stay zero)
@@ -312,12 +370,11 @@ void upload_batch(Plan& P, GemmBatch& g, const std::vector<int2>& h_items);
 void run_eval(Plan& P, const double* d_src, double* d_out);  // kafmm_eval.cu
 void run_eval_up(Plan& P, const double* d_src);               // a1-a4
 void run_eval_down(Plan& P, double* d_out);                   // a5-a12
-void restrict_plan(Plan& P, int64_t plo, int64_t phi);        // kafmm_dist.cu
 void build_m2l_batch(Plan& P);                                // kafmm_dist.cu
-void pack_ue(Plan& P, const int32_t* ids, int64_t n, double* buf);
-void unpack_ue(Plan& P, const int32_t* ids, int64_t n, const double* buf);
-void gather_rows(Plan& P, const double* src, int ld, const int64_t* idx, int64_t n, double* dst);
-void scatter_rows(Plan& P, const double* src, int ld, const int64_t* idx, int64_t n, double* dst);
+void setup_dist(Plan& P, const double* d_local_points, int64_t n_local);  // kafmm_dist.cu (P.dist->comm set)
+void run_eval_dist(Plan& P, const double* d_local_src, double* d_local_out);
+void alloc_workspaces(Plan& P);                               // kafmm_capi.cu
+void build_plan_core(Plan& P, const double* d_points);        // kafmm_capi.cu: tree, lists, operators, batches
 void check_values(Plan& P, const double* d_src);
 void take_nonfinite(Plan& P);             // kafmm_eval.cu
 void launch_gemm(Plan& P, const GemmBatch& g, const double* A, int M, int K, int lda,

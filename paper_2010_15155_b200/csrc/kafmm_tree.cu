@@ -697,7 +697,18 @@ void build_tree_and_lists(Plan& P, const double* d_points) {
 }
 
 // GEMM work lists of the per-box translations -----------------------------
-void upload_batch(Plan& P, GemmBatch& g, const std::vector<int2>& items) {
+// items are (input box, output box); on a partitioned plan they become heavy rows
+void upload_batch(Plan& P, GemmBatch& g, const std::vector<int2>& box_items) {
+  std::vector<int2> mapped;
+  if (!P.h_row.empty()) {
+    mapped.reserve(box_items.size());
+    for (const int2& it : box_items) {
+      const int2 r = make_int2(P.h_row[it.x], P.h_row[it.y]);
+      if (r.x < 0 || r.y < 0) throw Error{KAFMM_ECUDA, "GEMM item on a box without a row (partition bookkeeping)"};
+      mapped.push_back(r);
+    }
+  }
+  const std::vector<int2>& items = P.h_row.empty() ? box_items : mapped;
   g.n_items = (int64_t)items.size();
   g.d_items = dalloc<int2>(P, std::max<size_t>(1, items.size()));
   if (!items.empty())

@@ -1,29 +1,34 @@
 """Multi-GPU evaluation of the KAFMM sum.
 
+The product path is in libkafmm (csrc/kafmm_dist.cu, kafmm_comm.cu): the C ABI
+kafmm_setup_dist / kafmm_eval with NCCL inside (``dist_plan`` below), or the
+in-process test transport (``LocalDist``).  This module also holds the host
+logic of the partition and exchange in plain numpy -- the specification the
+C++ implementation follows and the GPU tests compare it with -- and the
+transport-generic driver ``spmd_eval`` that tests/test_dist_host.py runs on gloo
+process groups with the oracle's arithmetic per rank.
+
 One process per GPU.  The octree is split into contiguous Morton ranges of
 the sorted points (whole leaves), weighted by the work each point brings
 (P2P pairs, W/X surface evaluations, S2M, M2L pairs).  Every rank builds the
-same global tree and lists (kafmm_setup on the all-gathered points) and then
-restricts its plan to its range (kafmm_restrict).  An evaluation is
+same global tree and lists from the all-gathered points and keeps what its
+range needs.  An evaluation is
 
     E1  all-to-all-v  source values, from the caller's rows to every rank that
                       needs them (its owned points and the remote leaves of
                       its U and X lists)
-        kafmm_eval_up       S2M, UC2UE over owned leaves, M2M into active boxes
+        up pass       S2M, UC2UE over owned leaves, M2M into active boxes
     E2  all-reduce    UE of the boxes that straddle ranks (partial sums)
     E3  all-to-all-v  ghost UE: remote boxes named by the V lists of this
                       rank's active boxes and the W lists of its leaves
-        kafmm_eval_down     M2L, S2L, DC2DE, L2L, L2T, M2T, P2P, scatter
+        down pass     M2L, S2L, DC2DE, L2L, L2T, M2T, P2P, scatter
     E4  all-to-all-v  outputs, from the owning rank back to the caller's rows
 
-The exchange maps are host logic here: deterministic numpy functions of the
-global tree, so every rank derives the same send and receive lists without
-communicating them.  The collectives go through a Transport:
-TorchTransport (torch.distributed -- NCCL on GPUs, gloo in the CPU tests) or
-LocalTransport (all ranks in one process, e.g. several restricted plans on
-one GPU, run one after the other).  Packing and unpacking are library
-kernels (kafmm_pack_ue, kafmm_gather_rows, ...); nothing here computes the
-method's arithmetic.
+The exchange maps are deterministic functions of the global tree, so every
+rank derives the same send and receive lists without communicating them.
+In ``spmd_eval`` the collectives go through a Transport: TorchTransport
+(torch.distributed; gloo in the CPU tests) or LocalTransport (all ranks in one
+process); nothing here computes the method's arithmetic.
 """
 from __future__ import annotations
 
@@ -223,100 +228,6 @@ class TorchTransport:
         return [b]
 
 
-# ---------------------------------------------------------------------------
-# one rank's side of the exchange, on the GPU plan
-# ---------------------------------------------------------------------------
-class RankPlan:
-    """A restricted plan plus its exchange lists as device index tensors."""
-
-    def __init__(self, plan, maps: RankMaps, n_local: int):
-        import torch
-        self.plan, self.maps, self.n_local = plan, maps, n_local
-        inf = plan.info()
-        self.k_s, self.k_t, self.neq, self.n = inf.k_s, inf.k_t, inf.n_equiv, inf.n_points
-        dev = torch.device("cuda", torch.cuda.current_device())
-        i64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int64), device=dev)  # noqa: E731
-        i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)  # noqa: E731
-        self.val_send = [i64(a) for a in maps.val_send]
-        self.val_recv = [i64(a) for a in maps.val_recv]
-        self.out_send = [i64(a) for a in maps.out_send]
-        self.out_recv = [i64(a) for a in maps.out_recv]
-        self.ue_send = [i32(a) for a in maps.ue_send]
-        self.ue_recv = [i32(a) for a in maps.ue_recv]
-        self.shared = i32(maps.shared)
-        self.gvals = torch.zeros((self.n, self.k_s), dtype=torch.float64, device=dev)
-        self.gout = torch.zeros((self.n, self.k_t), dtype=torch.float64, device=dev)
-        self.dev = dev
-
-    def _rows(self, src, idx, width):
-        import torch
-        dst = torch.empty((idx.numel(), width), dtype=torch.float64, device=self.dev)
-        if idx.numel():
-            self.plan.gather_rows(src, idx, dst)
-        return dst
-
-    def _boxes(self, ids):
-        import torch
-        buf = torch.empty((ids.numel(), self.neq), dtype=torch.float64, device=self.dev)
-        if ids.numel():
-            self.plan.pack_ue(ids, buf)
-        return buf
-
-    # E1
-    def pack_values(self, local_vals):
-        return [self._rows(local_vals, i, self.k_s) for i in self.val_send]
-
-    def values_rows(self):
-        return [int(i.numel()) for i in self.val_recv]
-
-    def unpack_values(self, recv):
-        for buf, idx in zip(recv, self.val_recv):
-            if idx.numel():
-                self.plan.scatter_rows(buf.contiguous(), idx, self.gvals)
-
-    def up(self):
-        self.plan.eval_up(self.gvals)
-
-    # E2 / E3
-    def pack_shared(self):
-        return self._boxes(self.shared)
-
-    def unpack_shared(self, buf):
-        if self.shared.numel():
-            self.plan.unpack_ue(self.shared, buf.contiguous())
-
-    def pack_ghost(self):
-        return [self._boxes(i) for i in self.ue_send]
-
-    def ghost_rows(self):
-        return [int(i.numel()) for i in self.ue_recv]
-
-    def unpack_ghost(self, recv):
-        for buf, ids in zip(recv, self.ue_recv):
-            if ids.numel():
-                self.plan.unpack_ue(ids, buf.contiguous())
-
-    def down(self):
-        self.plan.eval_down(self.gout)
-
-    # E4
-    def pack_out(self):
-        return [self._rows(self.gout, i, self.k_t) for i in self.out_send]
-
-    def out_rows(self):
-        return [int(i.numel()) for i in self.out_recv]
-
-    def unpack_out(self, recv, local_out):
-        for buf, idx in zip(recv, self.out_recv):
-            if idx.numel():
-                self.plan.scatter_rows(buf.contiguous(), idx, local_out)
-        return local_out
-
-    def new_out(self):
-        import torch
-        return torch.empty((self.n_local, self.k_t), dtype=torch.float64, device=self.dev)
-
-
 def spmd_eval(ranks, transport, local_vals):
     """One distributed evaluation over the ranks of this process (all of
     them for LocalTransport, one for TorchTransport)."""
@@ -335,54 +246,74 @@ def spmd_eval(ranks, transport, local_vals):
     return [r.unpack_out(o, r.new_out()) for r, o in zip(ranks, outs)]
 
 
-def build_rank(global_points, caller_offsets, rank, world, kernel, p, cap, stream=None, weights=None):
-    """Set up rank `rank` of `world` on the current GPU."""
-    from .kafmm import KAFMM
-    plan = KAFMM(global_points, kernel, p, cap, stream=stream)
-    T = tree_from_plan(plan)
-    cuts = partition(T, world, weights)
-    maps = rank_maps(T, cuts, np.asarray(caller_offsets, dtype=np.int64), rank)
-    plan.restrict(maps.plo, maps.phi)
-    n_local = int(caller_offsets[rank + 1] - caller_offsets[rank])
-    rp = RankPlan(plan, maps, n_local)
-    rp.work = local_work(T, maps.plo, maps.phi)
-    return rp, cuts
+def dist_plan(local_points, kernel: str, p: int, cap: int, group=None, stream=None):
+    """This process's rank of a partitioned plan over torch.distributed's ranks
+    (one GPU each): rank 0 makes the NCCL id, torch.distributed broadcasts it,
+    and libkafmm sets up its own NCCL communicator (kafmm_setup_dist)."""
+    import torch
+    import torch.distributed as dist
+    from .kafmm import DistKAFMM, unique_id
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    buf = torch.zeros(128, dtype=torch.uint8, device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(unique_id()), dtype=torch.uint8))
+    dist.broadcast(buf, src=0, group=group)
+    return DistKAFMM(local_points, kernel, p, cap, rank=rank, world=world, nccl_id=bytes(buf.cpu().numpy()),
+                     stream=stream)
 
 
-def local_work(T: GlobalTree, plo: int, phi: int) -> dict:
-    """V pairs and P2P pairs this rank's restricted plan evaluates."""
-    active = (T.pbeg < phi) & (T.pend > plo)
-    vt, _ = T.lists["V"]
-    ut, us = T.lists["U"]
-    npts = T.pend - T.pbeg
-    m = active[ut]
-    return {"n_v": int(active[vt].sum()), "n_p2p": int((npts[ut[m]] * npts[us[m]]).sum())}
+def _run_threads(fns):
+    import threading
+    res, err = [None] * len(fns), []
+
+    def run(i):
+        try:
+            res[i] = fns[i]()
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(len(fns))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return res
 
 
-class DistKAFMM:
-    """The distributed evaluation for this process's rank (torch.distributed
-    initialised, one GPU per process).  local_points: this rank's rows."""
+class LocalDist:
+    """All ranks of a partitioned plan in this process, one host thread per rank
+    on the current GPU (kafmm_comm_local_create): the test transport of the
+    C-ABI multi-GPU path.  points[r] / values[r]: rank r's caller rows."""
 
-    def __init__(self, local_points, kernel: str, p: int, cap: int, group=None, stream=None):
+    def __init__(self, points, kernel: str, p: int, cap: int):
         import torch
-        import torch.distributed as dist
-        self.transport = TorchTransport(group)
-        rank, world = dist.get_rank(group), dist.get_world_size(group)
-        pts = torch.as_tensor(np.ascontiguousarray(local_points, dtype=np.float64)).cuda() \
-            if isinstance(local_points, np.ndarray) else local_points.to("cuda", torch.float64).contiguous()
-        cnt = torch.tensor([pts.shape[0]], dtype=torch.int64, device="cuda")
-        counts = [torch.zeros_like(cnt) for _ in range(world)]
-        dist.all_gather(counts, cnt, group=group)
-        counts = [int(c.item()) for c in counts]
-        mx = max(counts)
-        pad = torch.zeros((mx, 3), dtype=torch.float64, device="cuda")
-        pad[:pts.shape[0]] = pts
-        allp = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(allp, pad, group=group)
-        gpts = torch.cat([a[:c] for a, c in zip(allp, counts)])
-        offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-        self.rank, self.world = rank, world
-        self.ctx, self.cuts = build_rank(gpts, offsets, rank, world, kernel, p, cap, stream=stream)
+        from .kafmm import DistKAFMM, LocalComms
+        self.world = len(points)
+        self.comms = LocalComms(self.world)
+        dev = torch.cuda.current_device()
 
-    def eval(self, local_vals):
-        return spmd_eval([self.ctx], self.transport, [local_vals.contiguous()])[0]
+        def mk(r):
+            torch.cuda.set_device(dev)
+            return DistKAFMM(points[r], kernel, p, cap, comm=self.comms.handles[r])
+
+        self.plans = _run_threads([lambda r=r: mk(r) for r in range(self.world)])
+
+    def eval(self, values):
+        import torch
+        dev = torch.cuda.current_device()
+
+        def ev(r):
+            torch.cuda.set_device(dev)
+            out = self.plans[r].eval(values[r])
+            self.plans[r].sync()
+            return out
+
+        return _run_threads([lambda r=r: ev(r) for r in range(self.world)])
+
+    def close(self):
+        for pl in self.plans:
+            pl.close()
+        self.plans = []
+        self.comms.close()

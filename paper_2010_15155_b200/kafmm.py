@@ -69,13 +69,14 @@ _SIGS = [
     ("kafmm_setup2", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int,
                                C.POINTER(C.c_void_p)]),
     ("kafmm_eval2", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
-    ("kafmm_restrict", C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
-    ("kafmm_eval_up", C.c_int, [C.c_void_p, C.c_void_p]),
-    ("kafmm_eval_down", C.c_int, [C.c_void_p, C.c_void_p]),
-    ("kafmm_pack_ue", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
-    ("kafmm_unpack_ue", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
-    ("kafmm_gather_rows", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
-    ("kafmm_scatter_rows", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("kafmm_get_unique_id", C.c_int, [C.c_void_p]),
+    ("kafmm_setup_dist", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                   C.POINTER(C.c_void_p)]),
+    ("kafmm_comm_local_create", C.c_int, [C.c_int, C.c_void_p]),
+    ("kafmm_comm_destroy", None, [C.c_void_p]),
+    ("kafmm_setup_dist_comm", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                        C.POINTER(C.c_void_p)]),
+    ("kafmm_dist_query", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     ("kafmm_wall_setup", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     ("kafmm_wall_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kafmm_wall_eval", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -245,34 +246,6 @@ class KAFMM:
         _check(self.lib.kafmm_get_m2l_mode(self.h, C.byref(m)), "kafmm_get_m2l_mode")
         return ["dense", "fft", "fft_blocks", "fft_pairs"][m.value]
 
-    # multi-GPU building blocks (dist.py)
-    def restrict(self, plo: int, phi: int):
-        _check(self.lib.kafmm_restrict(self.h, int(plo), int(phi)), "kafmm_restrict")
-
-    def eval_up(self, src):
-        _check(self.lib.kafmm_eval_up(self.h, C.c_void_p(src.data_ptr())), "kafmm_eval_up")
-
-    def eval_down(self, out):
-        _check(self.lib.kafmm_eval_down(self.h, C.c_void_p(out.data_ptr())), "kafmm_eval_down")
-
-    def pack_ue(self, ids, buf):
-        _check(self.lib.kafmm_pack_ue(self.h, C.c_void_p(ids.data_ptr()), int(ids.numel()),
-                                      C.c_void_p(buf.data_ptr())), "kafmm_pack_ue")
-
-    def unpack_ue(self, ids, buf):
-        _check(self.lib.kafmm_unpack_ue(self.h, C.c_void_p(ids.data_ptr()), int(ids.numel()),
-                                        C.c_void_p(buf.data_ptr())), "kafmm_unpack_ue")
-
-    def gather_rows(self, src, idx, dst):
-        _check(self.lib.kafmm_gather_rows(self.h, C.c_void_p(src.data_ptr()), int(src.shape[1]),
-                                          C.c_void_p(idx.data_ptr()), int(idx.numel()), C.c_void_p(dst.data_ptr())),
-               "kafmm_gather_rows")
-
-    def scatter_rows(self, src, idx, dst):
-        _check(self.lib.kafmm_scatter_rows(self.h, C.c_void_p(src.data_ptr()), int(dst.shape[1]),
-                                           C.c_void_p(idx.data_ptr()), int(idx.numel()), C.c_void_p(dst.data_ptr())),
-               "kafmm_scatter_rows")
-
     def set_graph(self, on: bool):
         """Replay evaluations from a captured CUDA graph (same src/out pointers)."""
         _check(self.lib.kafmm_set_graph(self.h, int(bool(on))), "kafmm_set_graph")
@@ -361,3 +334,92 @@ class KAFMM2(KAFMM):
             out = torch.empty((self.n_trg, self.k_t), dtype=torch.float64, device=src.device)
         _check(self.lib.kafmm_eval2(self.h, C.c_void_p(src.data_ptr()), C.c_void_p(out.data_ptr())), "kafmm_eval2")
         return out
+
+
+def unique_id() -> bytes:
+    """A new NCCL unique id (128 bytes) for kafmm_setup_dist; rank 0 makes it."""
+    lib = load_library()
+    buf = (C.c_ubyte * 128)()
+    _check(lib.kafmm_get_unique_id(buf), "kafmm_get_unique_id")
+    return bytes(buf)
+
+
+class LocalComms:
+    """kafmm_comm_local_create: `world` in-process communicators (test transport:
+    ranks are host threads of this process on one GPU)."""
+
+    def __init__(self, world: int):
+        self.lib = load_library()
+        arr = (C.c_void_p * world)()
+        _check(self.lib.kafmm_comm_local_create(int(world), arr), "kafmm_comm_local_create")
+        self.handles = [C.c_void_p(arr[i]) for i in range(world)]
+
+    def close(self):
+        for h in self.handles:
+            if h.value:
+                self.lib.kafmm_comm_destroy(h)
+        self.handles = []
+
+    def __del__(self):
+        if getattr(self, "handles", None):
+            self.close()
+
+
+DIST_KEYS = ("rank", "world", "n_global", "n_caller", "n_owned", "n_local", "n_ghost_points", "n_rows",
+             "n_ghost_boxes", "n_shared", "plan_bytes", "bytes_per_eval", "n_v_local", "n_p2p_local")
+
+
+class DistKAFMM(KAFMM):
+    """One rank of a partitioned plan (kafmm_setup_dist over NCCL, or
+    kafmm_setup_dist_comm over a LocalComms handle).  eval takes and returns
+    this caller's rows; all ranks must call it collectively."""
+
+    def __init__(self, local_points, kernel: str, p: int, max_pts: int, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None, comm=None, stream=None):
+        torch = _torch()
+        self.lib = load_library()
+        self.kernel = kernel
+        if isinstance(local_points, np.ndarray):
+            pts = torch.from_numpy(np.ascontiguousarray(local_points, dtype=np.float64).reshape(-1, 3)).cuda()
+        else:
+            pts = local_points.to(device="cuda", dtype=torch.float64).contiguous().reshape(-1, 3)
+        self.n = int(pts.shape[0])
+        self.k_s, self.k_t = kernel_dims(kernel)
+        h = C.c_void_p()
+        ptr = C.c_void_p(pts.data_ptr()) if self.n > 0 else C.c_void_p(0)
+        torch.cuda.synchronize()
+        if comm is not None:
+            _check(self.lib.kafmm_setup_dist_comm(ptr, self.n, KERNELS[kernel], int(p), int(max_pts), comm,
+                                                  C.byref(h)), "kafmm_setup_dist_comm")
+        else:
+            idb = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+            _check(self.lib.kafmm_setup_dist(ptr, self.n, KERNELS[kernel], int(p), int(max_pts), int(rank),
+                                             int(world), idb, C.byref(h)), "kafmm_setup_dist")
+        self.h = h
+        if stream is not None:
+            self.set_stream(stream)
+
+    def eval(self, src, out=None):
+        torch = _torch()
+        assert src.is_cuda and src.dtype == torch.float64 and src.shape == (self.n, self.k_s)
+        src = src.contiguous()
+        if out is None:
+            out = torch.empty((self.n, self.k_t), dtype=torch.float64, device=src.device)
+        sp = C.c_void_p(src.data_ptr()) if src.numel() else C.c_void_p(8)
+        op = C.c_void_p(out.data_ptr()) if out.numel() else C.c_void_p(8)
+        _check(self.lib.kafmm_eval(self.h, sp, op), "kafmm_eval")
+        return out
+
+    def dist_info(self) -> dict:
+        v = np.zeros(len(DIST_KEYS), np.int64)
+        _check(self.lib.kafmm_dist_query(self.h, 0, C.c_void_p(v.ctypes.data)), "kafmm_dist_query")
+        d = {k: int(x) for k, x in zip(DIST_KEYS, v)}
+        w = d["world"]
+        cuts = np.zeros(w + 1, np.int64)
+        _check(self.lib.kafmm_dist_query(self.h, 1, C.c_void_p(cuts.ctypes.data)), "kafmm_dist_query")
+        cnt = np.zeros(6 * w, np.int64)
+        _check(self.lib.kafmm_dist_query(self.h, 2, C.c_void_p(cnt.ctypes.data)), "kafmm_dist_query")
+        d["cuts"] = cuts
+        for i, k in enumerate(("val_send", "val_recv", "ue_send", "ue_recv", "out_send", "out_recv")):
+            d[k] = cnt[i * w:(i + 1) * w]
+        return d

@@ -74,3 +74,28 @@ def test_product_package_never_imports_the_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), f
                 assert "oracle/" not in src, f
+
+
+def test_dist_entry_points_host_side(lib):
+    """kafmm_get_unique_id (NCCL opened at run time), the in-process test
+    communicators, and argument checks of kafmm_setup_dist -- host-only paths."""
+    import ctypes as C
+    buf = (C.c_ubyte * 128)()
+    st = lib.kafmm_get_unique_id(buf)
+    assert st in (0, 6), st  # 6 = ENCCL: no libnccl.so.2 in this environment
+    if st == 0:
+        assert any(bytes(buf))
+    h = C.c_void_p()
+    assert lib.kafmm_setup_dist(C.c_void_p(8), 10, 2, 8, 50, 2, 2, buf, C.byref(h)) == 1   # rank >= world
+    assert lib.kafmm_setup_dist(C.c_void_p(8), 10, 2, 8, 50, 0, 0, buf, C.byref(h)) == 1   # world < 1
+    assert lib.kafmm_setup_dist(C.c_void_p(8), 10, 2, 8, 50, 0, 1, None, C.byref(h)) == 1  # no id
+    assert h.value is None
+    arr = (C.c_void_p * 3)()
+    assert lib.kafmm_comm_local_create(3, arr) == 0
+    assert all(arr[i] for i in range(3))
+    assert lib.kafmm_setup_dist_comm(C.c_void_p(8), 10, 9, 8, 50, arr[0], C.byref(h)) == 1  # unknown kernel
+    for i in range(3):
+        lib.kafmm_comm_destroy(arr[i])
+    assert lib.kafmm_comm_local_create(0, arr) == 1
+    out = (C.c_int64 * 16)()
+    assert lib.kafmm_dist_query(None, 0, out) == 1
