@@ -614,6 +614,252 @@ __global__ void __launch_bounds__(SP_WARPS * 32, 1)
   }
 }
 
+// The sparse-chunk product over a precomputed item stream (the default for sparse
+// chunks).  Same arithmetic and table as k_m2l_sparse; what changes is how a warp
+// finds its work.  Per chunk, setup lists for every target parent P its items
+// (d, c): a non-leaf colleague Q_d and an existing child c of it such that some
+// existing child b of P is a V-list target of c, with
+//     vmask = { b : b exists, 2d + c - b non-adjacent }   (8 bits),
+// stored as int2 {q, d | c << 5 | vmask << 8}, parents in chunk order (ioff: CSR).
+// A warp owns a contiguous run of parents and walks their items as one stream:
+// items and parent boundaries arrive 32 at a time (one coalesced load per lane,
+// broadcast by shuffles, the next batch in flight), and the source spectra of the
+// next item are loaded while the current one is applied, so no global load sits
+// between two items' multiply-adds (k_m2l_sparse walked the 26 directions with a
+// dependent nbr -> qpat -> ub load chain per direction: 2/3 of them empty on the
+// C5 sphere cloud, and long-scoreboard stalls were 1/3 of its samples,
+// profiles/r02_C5_sparse_ncu.txt).
+// 16-B shared-memory load through a 32-bit shared address (the generic-pointer form
+// re-derived the CTA's shared window -- S2UR SR_CgaCtaId, an XU-pipe op -- in front of
+// every b block; the XU pipe then ran at 3.5x its sustained rate in ncu)
+__device__ __forceinline__ double2 lds_f64x2(unsigned a) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+
+// Signs per item.  For an item (d, c) every target child b sees o = 2d + c - b with the
+// same sign choice S = diag(sx, sy, sz): along an axis with d_k != 0 the sign of o_k is
+// that of d_k for every b; along an axis with d_k = 0, o_k = c_k - b_k is in {0, 1} when
+// c_k = 1 (take +) and in {-1, 0} when c_k = 0 (take -), and o_k = 0 admits either sign
+// (the kernel grid of such an offset is symmetric under that axis's reflection).  So the
+// reflection slot and the sign pattern of S [conj] T S are uniform over the item; setup
+// stores S in bits 16-18 of the item word and the product runs one of 8 code variants
+// with the signs folded into the multiply-adds (negated operands cost nothing), leaving
+// per block only the base-offset lookup and the six table loads.
+template <int KML, int SP>
+__device__ __forceinline__ void sparse_block_s(double2 (&o)[KML], const double2 (&U)[KML], unsigned t) {
+  constexpr bool SX = SP & 1, SY = (SP >> 1) & 1, SZ = (SP >> 2) & 1;  // true = negative
+  constexpr double cj = SZ ? -1.0 : 1.0;                                  // conj: imaginary parts
+  if (KML == 1) {
+    const double2 t0 = lds_f64x2(t);
+    cmac(o[0], make_double2(t0.x, cj * t0.y), U[0]);
+  } else {
+    constexpr double sxy = (SX != SY) ? -1.0 : 1.0, sxz = (SX != SZ) ? -1.0 : 1.0, syz = (SY != SZ) ? -1.0 : 1.0;
+    double2 T[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) T[k] = lds_f64x2(t + k * 32 * 16);
+    const double2 T0 = make_double2(T[0].x, cj * T[0].y), T3 = make_double2(T[3].x, cj * T[3].y),
+                  T5 = make_double2(T[5].x, cj * T[5].y);
+    const double2 T1 = make_double2(sxy * T[1].x, sxy * cj * T[1].y),
+                  T2 = make_double2(sxz * T[2].x, sxz * cj * T[2].y),
+                  T4 = make_double2(syz * T[4].x, syz * cj * T[4].y);
+    cmac(o[0], T0, U[0]);
+    cmac(o[0], T1, U[KML > 1 ? 1 : 0]);
+    cmac(o[0], T2, U[KML > 2 ? 2 : 0]);
+    cmac(o[KML > 1 ? 1 : 0], T1, U[0]);
+    cmac(o[KML > 1 ? 1 : 0], T3, U[KML > 1 ? 1 : 0]);
+    cmac(o[KML > 1 ? 1 : 0], T4, U[KML > 2 ? 2 : 0]);
+    cmac(o[KML > 2 ? 2 : 0], T2, U[0]);
+    cmac(o[KML > 2 ? 2 : 0], T4, U[KML > 1 ? 1 : 0]);
+    cmac(o[KML > 2 ? 2 : 0], T5, U[KML > 2 ? 2 : 0]);
+  }
+}
+
+// all blocks of one item with sign pattern SP: target children in pairs (b, b + 1), two
+// independent blocks (12 multiply-add chains) in flight when both are valid
+template <int KML, int NB, int SP>
+__device__ __forceinline__ void sparse_item_s(double2 (&acc)[NB][KML], const double2 (&U)[KML], unsigned vm,
+                                              const uint16_t* inf, unsigned tslot) {
+  constexpr unsigned OB = (KML == 1 ? 1 : 6) * 32 * 16;  // bytes per base offset
+#pragma unroll
+  for (int b = 0; b < NB; b += 2) {
+    const unsigned two = (vm >> b) & 3u;
+    if (two == 3u) {
+      const unsigned t0 = tslot + (inf[b * 8] & 63u) * OB, t1 = tslot + (inf[(b + 1) * 8] & 63u) * OB;
+      sparse_block_s<KML, SP>(acc[b], U, t0);
+      sparse_block_s<KML, SP>(acc[b + 1], U, t1);
+    } else if (two == 1u) {
+      sparse_block_s<KML, SP>(acc[b], U, tslot + (inf[b * 8] & 63u) * OB);
+    } else if (two == 2u) {
+      sparse_block_s<KML, SP>(acc[b + 1], U, tslot + (inf[(b + 1) * 8] & 63u) * OB);
+    }
+  }
+}
+
+template <int KML, int NB>
+__device__ __forceinline__ void sparse_apply(double2 (&acc)[NB][KML], const double2 (&U)[KML], int2 it,
+                                             unsigned sT32, int rs, int boff) {
+  const int dd = it.y & 31, c = (it.y >> 5) & 7;
+  const unsigned vm = ((unsigned)it.y >> 8) & 255u, sp = ((unsigned)it.y >> 16) & 7u;
+  const uint16_t* inf = c_pinfo + dd * 64 + boff * 8 + c;
+  // reflection of the item: fx iff sx != sz, fy iff sy != sz
+  const unsigned r = ((sp ^ (sp >> 2)) & 1u) | ((((sp >> 1) ^ (sp >> 2)) & 1u) << 1);
+  const unsigned tslot = sT32 + (unsigned)(((rs >> (5 * r)) & 31) * 16);
+  switch (KML == 1 ? (sp & 4u) : sp) {
+    case 0: sparse_item_s<KML, NB, 0>(acc, U, vm, inf, tslot); break;
+    case 1: sparse_item_s<KML, NB, 1>(acc, U, vm, inf, tslot); break;
+    case 2: sparse_item_s<KML, NB, 2>(acc, U, vm, inf, tslot); break;
+    case 3: sparse_item_s<KML, NB, 3>(acc, U, vm, inf, tslot); break;
+    case 4: sparse_item_s<KML, NB, 4>(acc, U, vm, inf, tslot); break;
+    case 5: sparse_item_s<KML, NB, 5>(acc, U, vm, inf, tslot); break;
+    case 6: sparse_item_s<KML, NB, 6>(acc, U, vm, inf, tslot); break;
+    default: sparse_item_s<KML, NB, 7>(acc, U, vm, inf, tslot); break;
+  }
+}
+
+#ifndef KF_ITEM_PF
+#define KF_ITEM_PF 6
+#endif
+constexpr int ITEM_PF = KF_ITEM_PF;  // items ahead whose source spectra are prefetched into L2
+
+// NB = 8: a warp's unit is a target parent (all 8 children in registers, 12 warps);
+// NB = 4: a half parent (children 4h .. 4h + 3, h = the x bit of the octant; ord carries
+// 2P + h), half the accumulators, 16 warps per SM -- the source spectra of an item are
+// loaded once per half
+template <int NB>
+struct ItemCfg {
+  static constexpr int WARPS = NB == 8 ? SP_WARPS : 16;
+};
+
+template <int KML, int NB>
+__global__ void __launch_bounds__(ItemCfg<NB>::WARPS * 32, 1)
+    k_m2l_items(int64_t npar, int64_t nq, int NFP, int nrange, const double2* __restrict__ tbase,
+                const int* __restrict__ rslot, const double2* __restrict__ ub, double2* __restrict__ cb,
+                const int32_t* __restrict__ ioff, const int2* __restrict__ items, const uint8_t* __restrict__ tpat,
+                const int32_t* __restrict__ wrange, const int32_t* __restrict__ ord) {
+  constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
+  extern __shared__ __align__(16) double2 sTb[];  // [N_BASE][NC][32]
+  const int g = blockIdx.y;
+  {
+    const double4* src = reinterpret_cast<const double4*>(tbase + (int64_t)g * N_BASE * NC * 32);
+    double4* dst = reinterpret_cast<double4*>(sTb);
+    for (int i = threadIdx.x; i < N_BASE * NC * 16; i += ItemCfg<NB>::WARPS * 32) dst[i] = src[i];
+  }
+  __syncthreads();
+  unsigned sT32;  // produced after the barrier (volatile), so no table read moves above it
+  asm volatile("mov.u32 %0, %1;" : "=r"(sT32) : "r"((unsigned)__cvta_generic_to_shared(sTb)));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rs = rslot[g * 32 + lane];
+  const double2* ubg = ub + (int64_t)g * nq * R * 32;
+  // the warp's parents: positions [wrange[r], wrange[r + 1]) of the processing order ord
+  // (setup deals the chunk's parents round-robin to the nrange warps of a frequency group,
+  // so at any time the running warps share a window of Morton-adjacent parents and the
+  // source spectra they read stay in L2)
+  const int r = blockIdx.x * ItemCfg<NB>::WARPS + warp;
+  if (r >= nrange) return;
+  const int pa = wrange[r], pe = wrange[r + 1];
+  // parent boundaries, ids and patterns, 32 positions per batch: lane l holds
+  // ioff[pb + l + 1], ord[pb + l] and its pattern
+  int pb = pa;
+  int pend = ioff[min(pb + lane + 1, pe)];
+  // unit id (parent, or 2 parent + half) and its child pattern (NB bits)
+  auto unit_pat = [&](int id) {
+    return NB == 8 ? (unsigned)tpat[id] : ((unsigned)tpat[id >> 1] >> (4 * (id & 1))) & 15u;
+  };
+  int pid = pb + lane < pe ? ord[pb + lane] : 0;
+  unsigned ppat = pb + lane < pe ? unit_pat(pid) : 0u;
+  const int ibeg = ioff[pa], iend = ioff[pe];
+  // item batches: lane l holds items[ib + l] (bat) and items[ib + 32 + l] (batn)
+  int ib = ibeg;
+  int2 bat = ib + lane < iend ? items[ib + lane] : make_int2(0, 0);
+  int2 batn = ib + 32 + lane < iend ? items[ib + 32 + lane] : make_int2(0, 0);
+  auto item_at = [&](int j) {  // j in [ib, ib + 64), warp-uniform
+    const int k = j - ib;
+    const int2 src = k < 32 ? bat : batn;
+    return make_int2(__shfl_sync(0xffffffffu, src.x, k & 31), __shfl_sync(0xffffffffu, src.y, k & 31));
+  };
+  // the 3 rows of source child c of parent q: one contiguous run of KML x 32 x 16 B
+  auto ublock = [&](int2 t) { return ubg + ((int64_t)t.x * R + ((t.y >> 5) & 7) * KML) * 32; };
+  auto prefetch = [&](int j) {
+    if (j < iend) {
+      const double2* u = ublock(item_at(j));
+      if (lane < KML * 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(u + lane * 8));
+    }
+  };
+  double2 acc[NB][KML];
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int a = 0; a < KML; ++a) acc[b][a] = make_double2(0.0, 0.0);
+  int P = pa;
+  int boff = 0;  // first child of the current unit
+  int pcur_end = __shfl_sync(0xffffffffu, pend, 0);
+  // store the finished parent P (every existing child, zero if it had no items), next parent
+  auto flush = [&]() {
+    const unsigned bm = __shfl_sync(0xffffffffu, ppat, P - pb);
+    const int id = __shfl_sync(0xffffffffu, pid, P - pb);
+    double2* o = cb + ((int64_t)(NB == 8 ? id : id >> 1) * R + boff * KML) * NFP + g * 32 + lane;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if ((bm >> b) & 1u) {
+#pragma unroll
+        for (int a = 0; a < KML; ++a) o[(int64_t)(b * KML + a) * NFP] = acc[b][a];
+      }
+#pragma unroll
+      for (int a = 0; a < KML; ++a) acc[b][a] = make_double2(0.0, 0.0);
+    }
+    ++P;
+    if (P < pe && P - pb == 32) {
+      pb = P;
+      pend = ioff[min(pb + lane + 1, pe)];
+      pid = pb + lane < pe ? ord[pb + lane] : 0;
+      ppat = pb + lane < pe ? unit_pat(pid) : 0u;
+    }
+    if (P < pe) {
+      pcur_end = __shfl_sync(0xffffffffu, pend, P - pb);
+      if (NB == 4) boff = 4 * (__shfl_sync(0xffffffffu, pid, P - pb) & 1);
+    }
+  };
+  if (NB == 4) boff = 4 * (__shfl_sync(0xffffffffu, pid, 0) & 1);
+  double2 U[KML];
+  int2 it = make_int2(0, 0);
+  if (ibeg < iend) {
+    for (int j = ibeg + 1; j <= ibeg + ITEM_PF; ++j) prefetch(j);
+    it = item_at(ibeg);
+    const double2* uq = ublock(it) + lane;
+#pragma unroll
+    for (int e = 0; e < KML; ++e) U[e] = uq[e * 32];
+  }
+  for (int i = ibeg; i < iend; ++i) {
+    while (i == pcur_end) flush();  // parents ending here (also those without items)
+    // next item and its source spectra, in flight during this item's products; the
+    // spectra ITEM_PF items ahead are pulled into L2
+    const int j = i + 1;
+    if (j - ib == 32) {
+      ib = j;
+      bat = batn;
+      batn = ib + 32 + lane < iend ? items[ib + 32 + lane] : make_int2(0, 0);
+    }
+    prefetch(i + ITEM_PF);
+    int2 nx = it;
+    double2 Un[KML];
+#pragma unroll
+    for (int e = 0; e < KML; ++e) Un[e] = U[e];
+    if (j < iend) {
+      nx = item_at(j);
+      const double2* uq = ublock(nx) + lane;
+#pragma unroll
+      for (int e = 0; e < KML; ++e) Un[e] = uq[e * 32];
+    }
+    sparse_apply<KML, NB>(acc, U, it, sT32, rs, boff);
+    it = nx;
+#pragma unroll
+    for (int e = 0; e < KML; ++e) U[e] = Un[e];
+  }
+  while (P < pe) flush();
+}
+
 // base table of the sparse product: tbase[g][ob][c][s] = That_{o(ob)}(f(g, s))[c] (0 on padding slots)
 __global__ void k_tbase(int nfg, int nc, const int32_t* __restrict__ gfreq, const int16_t* __restrict__ boff,
                         const double2* __restrict__ that, double2* __restrict__ tbase) {
@@ -708,6 +954,13 @@ bool fft_supported_p(int p) { return (p >= 3 && p <= 8) || p == 10 || p == 12; }
 #endif
 constexpr int NT_L = KF_NT_L, NT_G = KF_NT_G;  // parent n-tiles per warp (Laplace, Stokes family); measured best (profiles/)
 
+// target children per warp unit of the sparse product: 8 (whole parent) or 4 (half parent);
+// KAFMM_ITEM_NB=4|8 overrides (tuning knob, read at plan setup and launch)
+int item_nb() {
+  static const int v = getenv("KAFMM_ITEM_NB") ? (atoi(getenv("KAFMM_ITEM_NB")) == 4 ? 4 : 8) : 8;
+  return v;
+}
+
 void run_m2l_fft(Plan& Pl) {
   for (const FftChunk& ch : Pl.fft_chunks) {
     if (ch.nt == 0 || ch.nq == 0) continue;
@@ -727,6 +980,33 @@ void run_m2l_fft(Plan& Pl) {
         KF_CUDA(cudaFuncSetAttribute(k_m2l_sparse<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(N_BASE * 6 * 32 * sizeof(double2))));
       }
+      static const bool dirs = getenv("KAFMM_SPARSE_DIRS") != nullptr;  // A/B knob: the direction walk
+      if (!dirs) {
+        static std::atomic<uint64_t> attr2{0};
+        if (first_on_device(attr2)) {
+          for (auto fn : {k_m2l_items<1, 8>, k_m2l_items<1, 4>})
+            KF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(N_BASE * 32 * sizeof(double2))));
+          for (auto fn : {k_m2l_items<3, 8>, k_m2l_items<3, 4>})
+            KF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(N_BASE * 6 * 32 * sizeof(double2))));
+        }
+        const int nb = item_nb();
+        const int wpc = nb == 8 ? ItemCfg<8>::WARPS : ItemCfg<4>::WARPS;
+        const dim3 grid((unsigned)std::max<int64_t>(1, (ch.nrange + wpc - 1) / wpc), (unsigned)Pl.NFG);
+#define KF_ITEMS(KML, NB)                                                                                      \
+  k_m2l_items<KML, NB><<<grid, wpc * 32, smem, Pl.stream>>>(ch.npar, ch.nq, Pl.NFP, (int)ch.nrange, Pl.d_tbase, \
+                                                           Pl.d_rslot, Pl.d_ub, Pl.d_cb, ch.d_ioff, ch.d_items,  \
+                                                           ch.d_tpat, ch.d_wrange, ch.d_ord)
+        if (Pl.kml == 1) {
+          if (nb == 8) KF_ITEMS(1, 8);
+          else KF_ITEMS(1, 4);
+        } else {
+          if (nb == 8) KF_ITEMS(3, 8);
+          else KF_ITEMS(3, 4);
+        }
+#undef KF_ITEMS
+      } else {
       const int64_t per_cta = (int64_t)SP_WARPS * 16;
       const dim3 grid((unsigned)std::max<int64_t>(1, (ch.npar + per_cta - 1) / per_cta), (unsigned)Pl.NFG);
       if (Pl.kml == 1)
@@ -735,6 +1015,7 @@ void run_m2l_fft(Plan& Pl) {
       else
         k_m2l_sparse<3><<<grid, SP_WARPS * 32, smem, Pl.stream>>>(ch.npar, ch.nq, Pl.NFP, Pl.d_tbase, Pl.d_rslot,
                                                                   Pl.d_ub, Pl.d_cb, ch.d_nbr, ch.d_tpat, ch.d_qpat);
+      }
     } else {
       // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
       // (fewer registers, more resident warps) -- a tuning knob measured in profiles/
@@ -1059,7 +1340,8 @@ void build_fft_chunks(Plan& P, int64_t budget) {
   const int64_t per_block = (int64_t)R * P.NFP * 16;  // one parent block of spectra
   for (FftChunk& c : P.fft_chunks)  // re-planning (kafmm_restrict): release the old lists
     for (void* p : {(void*)c.d_qbox, (void*)c.d_nbr, (void*)c.d_tbox, (void*)c.d_tpb, (void*)c.d_toff,
-                    (void*)c.d_tpat, (void*)c.d_qpat})
+                    (void*)c.d_tpat, (void*)c.d_qpat, (void*)c.d_ioff, (void*)c.d_items, (void*)c.d_wrange,
+                    (void*)c.d_ord})
       dfree(P, p);
   P.fft_chunks.clear();
   P.fft_max_nq = P.fft_max_npar = 0;
@@ -1164,6 +1446,86 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         int64_t blocks = 0;
         for (int32_t v : nb) blocks += v >= 0;
         ch.block_fill = blocks ? (double)ch.npairs / (64.0 * (double)blocks) : 1.0;
+      }
+      {  // item stream of the sparse product (k_m2l_items)
+        // items of every parent in chunk order
+        std::vector<int32_t> cnt(ch.npar, 0);
+        std::vector<int2> all;
+        for (int64_t q = 0; q < ch.npar; ++q) {
+          for (int dd = 0; dd < 26; ++dd) {
+            const int32_t qq = nb[q * 26 + dd];
+            if (qq < 0) continue;
+            const int d = dd < 13 ? dd : dd + 1;
+            for (int c = 0; c < 8; ++c) {
+              if (!((qpat[qq] >> c) & 1)) continue;
+              unsigned vm = 0;
+              for (int b = 0; b < 8; ++b) {
+                if (!((tpat[q] >> b) & 1)) continue;
+                const int ox = 2 * (d / 9 - 1) + ((c >> 2) & 1) - ((b >> 2) & 1);
+                const int oy = 2 * ((d / 3) % 3 - 1) + ((c >> 1) & 1) - ((b >> 1) & 1);
+                const int oz = 2 * (d % 3 - 1) + (c & 1) - (b & 1);
+                if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) >= 2) vm |= 1u << b;
+              }
+              if (vm) {
+                // sign pattern of the item (see sparse_apply): bit k set = axis k negative
+                const int dv[3] = {d / 9 - 1, (d / 3) % 3 - 1, d % 3 - 1};
+                int sp = 0;
+                for (int k = 0; k < 3; ++k) {
+                  const int ck = (c >> (2 - k)) & 1;
+                  if (dv[k] < 0 || (dv[k] == 0 && ck == 0)) sp |= 1 << k;
+                }
+                all.push_back(make_int2(qq, dd | (c << 5) | (int)(vm << 8) | (sp << 16)));
+                ++cnt[q];
+              }
+            }
+          }
+          if (all.size() >= (size_t)INT32_MAX) throw Error{KAFMM_EINVAL, "FFT M2L chunk: too many items"};
+        }
+        std::vector<int64_t> start(ch.npar + 1, 0);
+        for (int64_t q = 0; q < ch.npar; ++q) start[q + 1] = start[q] + cnt[q];
+        // processing order: the units (parents, or half parents when item_nb() == 4) dealt
+        // round-robin to W warps per frequency group (W = warps per CTA x CTAs per group, >= 4
+        // units per warp), warp slot s taking unit positions s, s + W, s + 2W, ...; ord / ioff /
+        // items follow that order, wrange cuts it per warp
+        const int nbu = item_nb(), halves = nbu == 8 ? 1 : 2;
+        const int64_t nunit = ch.npar * halves;
+        const int64_t wpc = nbu == 8 ? ItemCfg<8>::WARPS : ItemCfg<4>::WARPS;
+        const int64_t X = std::min<int64_t>(148, std::max<int64_t>(1, (nunit + wpc * 4 - 1) / (wpc * 4)));
+        const int64_t W = X * wpc;
+        std::vector<int32_t> ord, ioff(1, 0), wr(1, 0);
+        std::vector<int2> items;
+        ord.reserve(nunit);
+        items.reserve(all.size() * halves);
+        for (int64_t sl = 0; sl < W; ++sl) {
+          for (int64_t u = sl; u < nunit; u += W) {
+            const int64_t q = u / halves;
+            const int h = (int)(u % halves);
+            ord.push_back((int32_t)(halves == 1 ? q : 2 * q + h));
+            for (int64_t e = start[q]; e < start[q + 1]; ++e) {
+              int2 it = all[e];
+              if (halves == 2) {
+                const unsigned vm = (((unsigned)it.y >> 8) >> (4 * h)) & 15u;
+                if (!vm) continue;
+                it.y = (it.y & ~0xFF00) | (int)(vm << 8);
+              }
+              items.push_back(it);
+            }
+            ioff.push_back((int32_t)items.size());
+          }
+          wr.push_back((int32_t)ord.size());
+        }
+        ch.nitems = (int64_t)items.size();
+        ch.nrange = W;
+        ch.d_ioff = dalloc<int32_t>(P, ioff.size());
+        ch.d_ord = dalloc<int32_t>(P, std::max<size_t>(1, ord.size()));
+        ch.d_wrange = dalloc<int32_t>(P, wr.size());
+        ch.d_items = dalloc<int2>(P, std::max<size_t>(1, items.size()));
+        KF_CUDA(cudaMemcpyAsync(ch.d_ioff, ioff.data(), ioff.size() * 4, cudaMemcpyHostToDevice, st));
+        if (!ord.empty()) KF_CUDA(cudaMemcpyAsync(ch.d_ord, ord.data(), ord.size() * 4, cudaMemcpyHostToDevice, st));
+        KF_CUDA(cudaMemcpyAsync(ch.d_wrange, wr.data(), wr.size() * 4, cudaMemcpyHostToDevice, st));
+        if (!items.empty())
+          KF_CUDA(cudaMemcpyAsync(ch.d_items, items.data(), items.size() * 8, cudaMemcpyHostToDevice, st));
+        KF_CUDA(cudaStreamSynchronize(st));
       }
       ch.d_tpat = dalloc<uint8_t>(P, std::max<int64_t>(1, ch.npar));
       ch.d_qpat = dalloc<uint8_t>(P, std::max<int64_t>(1, ch.nq));

@@ -77,6 +77,14 @@ struct FftChunk {
   int64_t npairs = 0;           // V pairs of the chunk
   uint8_t* d_tpat = nullptr;    // npar
   uint8_t* d_qpat = nullptr;    // nq
+  // item stream of the sparse product (k_m2l_items): per target parent P the (colleague
+  // direction d, source child c) items with a non-empty target mask, CSR over parents
+  int32_t* d_ioff = nullptr;    // npar + 1, in processing order (d_ord)
+  int2* d_items = nullptr;      // {q, d | c << 5 | vmask << 8}
+  int64_t nitems = 0;
+  int32_t* d_ord = nullptr;     // npar: processing order of the parents (chunk-local ids)
+  int32_t* d_wrange = nullptr;  // nrange + 1: each warp's positions in that order
+  int64_t nrange = 0;
   double block_fill = 1.0;      // V pairs / (8x8 child blocks the DMMA product runs)
 };
 

@@ -19,6 +19,6 @@ for src in B.SOURCES:
     obj = os.path.join(bdir, src.replace(".cu", ".o"))
     subprocess.run([B.nvcc(), *B.ARCH, *B.FLAGS, *defs, "-c", os.path.join(B.CSRC, src), "-o", obj], check=True)
     objs.append(obj)
-subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", out, *objs, "-lcublas", "-lcusolver", "-lcufft", "-lcudart"],
+subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", out, *objs, "-lcublas", "-lcusolver", "-lcufft", "-lcudart", "-ldl"],
                check=True)
 print(out)
