@@ -43,6 +43,12 @@ static void free_plan(kafmm_plan_s* P) {
   if (P->ev_gout) cudaEventDestroy(P->ev_gout);
   if (P->ev_near_in) cudaEventDestroy(P->ev_near_in);
   if (P->ev_near_out) cudaEventDestroy(P->ev_near_out);
+  if (P->cstream) {
+    cudaStreamSynchronize(P->cstream);
+    cudaStreamDestroy(P->cstream);
+  }
+  if (P->ev_up) cudaEventDestroy(P->ev_up);
+  if (P->ev_ghost) cudaEventDestroy(P->ev_ghost);
   delete P->dist;
   delete P;
 }
@@ -138,6 +144,9 @@ void alloc_workspaces(Plan& P) {
   KF_CUDA(cudaEventCreateWithFlags(&P.ev_gout, cudaEventDisableTiming));
   KF_CUDA(cudaEventCreateWithFlags(&P.ev_near_in, cudaEventDisableTiming));
   KF_CUDA(cudaEventCreateWithFlags(&P.ev_near_out, cudaEventDisableTiming));
+  KF_CUDA(cudaStreamCreateWithFlags(&P.cstream, cudaStreamNonBlocking));
+  KF_CUDA(cudaEventCreateWithFlags(&P.ev_up, cudaEventDisableTiming));
+  KF_CUDA(cudaEventCreateWithFlags(&P.ev_ghost, cudaEventDisableTiming));
   KF_CUDA(cudaStreamSynchronize(P.stream));
 }
 }  // namespace kafmm

@@ -19,7 +19,9 @@
 //                     (it needs only E1) and overlaps E2, E3 and the down pass
 //   E2  all-reduce    UE of the boxes straddling ranks (partial sums)
 //   E3  all-to-all-v  ghost UE from each box's owner
-//       down pass     M2L, S2L, DC2DE, L2L, L2T, M2T, join P2P, scatter
+//                     (E2 and E3 run on a second stream; S2L, which needs only
+//                     the source records, runs meanwhile on the plan's stream)
+//       down pass     M2L, DC2DE, L2L, L2T, M2T, join P2P, scatter
 //   E4  all-to-all-v  outputs: owner -> caller rows
 // The collectives are NCCL (kafmm_comm.cu) on the plan's stream.  The host
 // logic follows the reference specification in paper_2010_15155_b200/dist.py
@@ -126,15 +128,15 @@ __global__ void k_scatter_rows64(const double* __restrict__ src, int ld, const i
   dst[idx[j] * ld + c] = src[t];
 }
 
-static void pack_rows(Plan& P, const int32_t* rows, int64_t n, double* buf) {
+static void pack_rows(Plan& P, const int32_t* rows, int64_t n, double* buf, cudaStream_t st) {
   if (n <= 0) return;
-  k_pack_rows32<<<nblk(n * P.neq), 256, 0, P.stream>>>(P.d_ue, P.ldn, rows, n, P.neq, buf);
+  k_pack_rows32<<<nblk(n * P.neq), 256, 0, st>>>(P.d_ue, P.ldn, rows, n, P.neq, buf);
   KF_CHECK_LAUNCH();
   P.launches++;
 }
-static void unpack_rows(Plan& P, const int32_t* rows, int64_t n, const double* buf) {
+static void unpack_rows(Plan& P, const int32_t* rows, int64_t n, const double* buf, cudaStream_t st) {
   if (n <= 0) return;
-  k_unpack_rows32<<<nblk(n * P.neq), 256, 0, P.stream>>>(P.d_ue, P.ldn, rows, n, P.neq, buf);
+  k_unpack_rows32<<<nblk(n * P.neq), 256, 0, st>>>(P.d_ue, P.ldn, rows, n, P.neq, buf);
   KF_CHECK_LAUNCH();
   P.launches++;
 }
@@ -679,17 +681,31 @@ void run_eval_dist(Plan& P, const double* d_src, double* d_out) {
               D.e1.rcount.data(), st);
   run_eval_up(P, D.e1.d_rbuf);  // P2P now runs on the side stream, overlapping E2 / E3
   int extra = 1;
+  // E2 and E3 on the exchange stream once the upward pass is done, while the plan's
+  // stream runs S2L (issued first, so that a host-blocking transport still overlaps);
+  // stage timing (mode 1) keeps everything on one stream in the original order
+  const bool overlap = P.timing != 1;
+  cudaStream_t xs = overlap ? P.cstream : st;
+  if (overlap) {
+    KF_CUDA(cudaEventRecord(P.ev_up, st));
+    run_eval_s2l(P);
+    KF_CUDA(cudaStreamWaitEvent(xs, P.ev_up, 0));
+  }
   // E2
   if (D.nshared > 0) {
-    pack_rows(P, D.d_shared_rows, D.nshared, D.d_shared_buf);
-    C.allreduce(D.d_shared_buf, D.nshared * P.neq, st);
-    unpack_rows(P, D.d_shared_rows, D.nshared, D.d_shared_buf);
+    pack_rows(P, D.d_shared_rows, D.nshared, D.d_shared_buf, xs);
+    C.allreduce(D.d_shared_buf, D.nshared * P.neq, xs);
+    unpack_rows(P, D.d_shared_rows, D.nshared, D.d_shared_buf, xs);
   }
   // E3
-  pack_rows(P, D.d_ue_send_rows, D.e3.stotal / P.neq, D.e3.d_sbuf);
+  pack_rows(P, D.d_ue_send_rows, D.e3.stotal / P.neq, D.e3.d_sbuf, xs);
   C.alltoallv(D.e3.d_sbuf, D.e3.sdispl.data(), D.e3.scount.data(), D.e3.d_rbuf, D.e3.rdispl.data(),
-              D.e3.rcount.data(), st);
-  unpack_rows(P, D.d_ue_recv_rows, D.e3.rtotal / P.neq, D.e3.d_rbuf);
+              D.e3.rcount.data(), xs);
+  unpack_rows(P, D.d_ue_recv_rows, D.e3.rtotal / P.neq, D.e3.d_rbuf, xs);
+  if (overlap) {
+    KF_CUDA(cudaEventRecord(P.ev_ghost, xs));
+    KF_CUDA(cudaStreamWaitEvent(st, P.ev_ghost, 0));
+  }
   const int up_launches = P.launches;
   run_eval_down(P, D.e4.d_sbuf);
   // E4

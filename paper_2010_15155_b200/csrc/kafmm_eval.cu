@@ -456,7 +456,9 @@ static void eval_down_impl(Plan& P, double* d_out) {
     if (P.timing == 1 || (P.timing == 2 && (s == ST_GATHER || s == ST_TOTAL))) KF_CUDA(cudaEventRecord(P.ev[s], st));
   };
   const Jobs& J = P.J;
-  KF_CUDA(cudaMemsetAsync(P.d_chk, 0, (size_t)P.nrow * P.ldn * 8, st));
+  const bool s2l_done = P.s2l_early;
+  P.s2l_early = false;
+  if (!s2l_done) KF_CUDA(cudaMemsetAsync(P.d_chk, 0, (size_t)P.nrow * P.ldn * 8, st));
   mark(ST_M2L);
   P.prod_used = 0;
   if (P.m2l_mode != M2L_DENSE) {
@@ -467,7 +469,7 @@ static void eval_down_impl(Plan& P, double* d_out) {
     prod_mark(P);
   }
   mark(ST_S2L);
-  if (J.nx > 0) launch_surface<KS, SREC, true>(P, J.x_tgt, J.nx, J.x_roff, J.x_rng, ALPHA_DC);
+  if (J.nx > 0 && !s2l_done) launch_surface<KS, SREC, true>(P, J.x_tgt, J.nx, J.x_roff, J.x_rng, ALPHA_DC);
   mark(ST_DC2DE);
   for (int l = 2; l <= P.depth; ++l) {
     int i = l - 2;
@@ -530,6 +532,28 @@ void run_eval_down(Plan& P, double* d_out) {
     case KAFMM_STOKES_REG_VEL_OMEGA: eval_down_impl<KGET, KGO, KGETW, 12>(P, d_out); break;
     case KAFMM_LAPLACE_PGRADGRAD: eval_down_impl<KLD, KLGG, KLDGG, 8>(P, d_out); break;
     case KAFMM_LAPLACE_QPGRADGRAD: eval_down_impl<KLQ, KLGG, KLQGG, 12>(P, d_out); break;
+    default: throw Error{KAFMM_EINVAL, "unknown kernel"};
+  }
+}
+
+// a6 ahead of a5: S2L needs only the gathered source records, so a partitioned
+// evaluation issues it before the ghost-multipole exchange completes
+template <class KS, int SREC>
+static void eval_s2l_impl(Plan& P) {
+  KF_CUDA(cudaMemsetAsync(P.d_chk, 0, (size_t)P.nrow * P.ldn * 8, P.stream));
+  if (P.J.nx > 0) launch_surface<KS, SREC, true>(P, P.J.x_tgt, P.J.nx, P.J.x_roff, P.J.x_rng, ALPHA_DC);
+  P.s2l_early = true;
+}
+
+void run_eval_s2l(Plan& P) {
+  switch (P.kernel) {
+    case KAFMM_LAPLACE_PGRAD: eval_s2l_impl<KL, 4>(P); break;
+    case KAFMM_STOKESLET: eval_s2l_impl<KG, 8>(P); break;
+    case KAFMM_RPY: eval_s2l_impl<KRPY, 8>(P); break;
+    case KAFMM_STOKES_REG_VEL: eval_s2l_impl<KGE, 8>(P); break;
+    case KAFMM_STOKES_REG_VEL_OMEGA: eval_s2l_impl<KGET, 12>(P); break;
+    case KAFMM_LAPLACE_PGRADGRAD: eval_s2l_impl<KLD, 8>(P); break;
+    case KAFMM_LAPLACE_QPGRADGRAD: eval_s2l_impl<KLQ, 12>(P); break;
     default: throw Error{KAFMM_EINVAL, "unknown kernel"};
   }
 }

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "kafmm_internal.h"
+#include "kafmm_spos.h"
 
 namespace kafmm {
 
@@ -405,16 +406,22 @@ constexpr int DM_WARPS = KF_DM_WARPS;
 #ifndef KF_DMMA_MINB3
 #define KF_DMMA_MINB3 4  // Stokes family: cap 128 registers, 4 CTAs per SM (C3 product -14%, profiles/r01_dmma_ab.txt)
 #endif
+__device__ const int16_t d_spos1[N_OFFSETS] = KF_SPOS1_INIT;
+__device__ const int16_t d_spos3[N_OFFSETS * 6] = KF_SPOS3_INIT;
+
 template <int KML, int NT>
 __global__ void __launch_bounds__(DM_WARPS * 32, KML == 1 ? KF_DMMA_MINB1 : KF_DMMA_MINB3)
     k_m2l_dmma(int64_t npar, int64_t nq, int npb, const double2* __restrict__ that, const double2* __restrict__ ub,
                double2* __restrict__ cb, const int32_t* __restrict__ nbr, const int16_t* __restrict__ aidx,
                const int16_t* __restrict__ fpos, int NFP) {
   constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML, KS = R / 4, PPW = NT * 8;
-  __shared__ double2 sT[N_OFFSETS * NC];
+  // the frequency's spectra at the bank-conflict-minimising positions of kafmm_spos.h
+  // (the A-fragment gather below reads them through aidx, which holds those positions)
+  __shared__ double2 sT[KML == 1 ? SPOS1_N : SPOS3_N];
+  const int16_t* spos = KML == 1 ? d_spos1 : d_spos3;
   const int64_t f = blockIdx.x / npb;
   const int pb = blockIdx.x % npb;
-  for (int i = threadIdx.x; i < N_OFFSETS * NC; i += DM_WARPS * 32) sT[i] = that[f * N_OFFSETS * NC + i];
+  for (int i = threadIdx.x; i < N_OFFSETS * NC; i += DM_WARPS * 32) sT[spos[i]] = that[f * N_OFFSETS * NC + i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
@@ -643,78 +650,85 @@ __device__ __forceinline__ double2 lds_f64x2(unsigned a) {
 // that of d_k for every b; along an axis with d_k = 0, o_k = c_k - b_k is in {0, 1} when
 // c_k = 1 (take +) and in {-1, 0} when c_k = 0 (take -), and o_k = 0 admits either sign
 // (the kernel grid of such an offset is symmetric under that axis's reflection).  So the
-// reflection slot and the sign pattern of S [conj] T S are uniform over the item; setup
-// stores S in bits 16-18 of the item word and the product runs one of 8 code variants
-// with the signs folded into the multiply-adds (negated operands cost nothing), leaving
-// per block only the base-offset lookup and the six table loads.
-template <int KML, int SP>
-__device__ __forceinline__ void sparse_block_s(double2 (&o)[KML], const double2 (&U)[KML], unsigned t) {
-  constexpr bool SX = SP & 1, SY = (SP >> 1) & 1, SZ = (SP >> 2) & 1;  // true = negative
-  constexpr double cj = SZ ? -1.0 : 1.0;                                  // conj: imaginary parts
+// reflection slot and the sign masks of S [conj] T S are uniform over the item: setup
+// stores S in bits 16-18 of the item word, the masks are formed once per item, and a
+// block costs the base-offset lookup, six table loads and the sign flips.  (One code
+// variant per sign pattern, with the flips folded into the multiply-adds, overflowed
+// the instruction cache: 2.4x slower, profiles/r02_C5_items_ncu.txt.)
+struct ItemSigns {
+  unsigned tslot;                            // shared address of the item's reflected bin slot
+  unsigned mc, mxy, mxyc, mxz, mxzc, myz, myzc;  // sign-bit masks (bit 31)
+};
+
+template <int KML>
+__device__ __forceinline__ void sparse_block(double2 (&o)[KML], const double2 (&U)[KML], unsigned t,
+                                             const ItemSigns& sg) {
   if (KML == 1) {
     const double2 t0 = lds_f64x2(t);
-    cmac(o[0], make_double2(t0.x, cj * t0.y), U[0]);
+    cmac(o[0], make_double2(t0.x, xsign(t0.y, sg.mc)), U[0]);
   } else {
-    constexpr double sxy = (SX != SY) ? -1.0 : 1.0, sxz = (SX != SZ) ? -1.0 : 1.0, syz = (SY != SZ) ? -1.0 : 1.0;
     double2 T[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) T[k] = lds_f64x2(t + k * 32 * 16);
-    const double2 T0 = make_double2(T[0].x, cj * T[0].y), T3 = make_double2(T[3].x, cj * T[3].y),
-                  T5 = make_double2(T[5].x, cj * T[5].y);
-    const double2 T1 = make_double2(sxy * T[1].x, sxy * cj * T[1].y),
-                  T2 = make_double2(sxz * T[2].x, sxz * cj * T[2].y),
-                  T4 = make_double2(syz * T[4].x, syz * cj * T[4].y);
-    cmac(o[0], T0, U[0]);
-    cmac(o[0], T1, U[KML > 1 ? 1 : 0]);
-    cmac(o[0], T2, U[KML > 2 ? 2 : 0]);
-    cmac(o[KML > 1 ? 1 : 0], T1, U[0]);
-    cmac(o[KML > 1 ? 1 : 0], T3, U[KML > 1 ? 1 : 0]);
-    cmac(o[KML > 1 ? 1 : 0], T4, U[KML > 2 ? 2 : 0]);
-    cmac(o[KML > 2 ? 2 : 0], T2, U[0]);
-    cmac(o[KML > 2 ? 2 : 0], T4, U[KML > 1 ? 1 : 0]);
-    cmac(o[KML > 2 ? 2 : 0], T5, U[KML > 2 ? 2 : 0]);
+    T[0].y = xsign(T[0].y, sg.mc);
+    T[3].y = xsign(T[3].y, sg.mc);
+    T[5].y = xsign(T[5].y, sg.mc);
+    T[1] = make_double2(xsign(T[1].x, sg.mxy), xsign(T[1].y, sg.mxyc));
+    T[2] = make_double2(xsign(T[2].x, sg.mxz), xsign(T[2].y, sg.mxzc));
+    T[4] = make_double2(xsign(T[4].x, sg.myz), xsign(T[4].y, sg.myzc));
+    cmac(o[0], T[0], U[0]);
+    cmac(o[0], T[1], U[KML > 1 ? 1 : 0]);
+    cmac(o[0], T[2], U[KML > 2 ? 2 : 0]);
+    cmac(o[KML > 1 ? 1 : 0], T[1], U[0]);
+    cmac(o[KML > 1 ? 1 : 0], T[3], U[KML > 1 ? 1 : 0]);
+    cmac(o[KML > 1 ? 1 : 0], T[4], U[KML > 2 ? 2 : 0]);
+    cmac(o[KML > 2 ? 2 : 0], T[2], U[0]);
+    cmac(o[KML > 2 ? 2 : 0], T[4], U[KML > 1 ? 1 : 0]);
+    cmac(o[KML > 2 ? 2 : 0], T[5], U[KML > 2 ? 2 : 0]);
   }
 }
 
-// all blocks of one item with sign pattern SP: target children in pairs (b, b + 1), two
-// independent blocks (12 multiply-add chains) in flight when both are valid
-template <int KML, int NB, int SP>
-__device__ __forceinline__ void sparse_item_s(double2 (&acc)[NB][KML], const double2 (&U)[KML], unsigned vm,
-                                              const uint16_t* inf, unsigned tslot) {
-  constexpr unsigned OB = (KML == 1 ? 1 : 6) * 32 * 16;  // bytes per base offset
+#ifndef KF_BPAIR
+#define KF_BPAIR 1
+#endif
+// all blocks of one item: target children in pairs (b, b + 1), two independent blocks
+// (12 multiply-add chains) in flight when both are valid.  Item word y (setup,
+// build_fft_chunks): bits 0-10 d * 64 + c (the c_pinfo row), 11-18 vmask, 19-20 the
+// reflection r, 29-31 the signs sx, sy, sz; slots4 packs the lane's 4 reflected slots.
+template <int KML, int NB>
+__device__ __forceinline__ void sparse_apply(double2 (&acc)[NB][KML], const double2 (&U)[KML], unsigned y,
+                                             unsigned sT32, unsigned slots4, int boff) {
+  constexpr unsigned OB = (KML == 1 ? 1 : 6) * 32 * 16;  // bytes per base offset in the table
+  const unsigned vm = (y >> 11) & 255u;
+  const uint16_t* inf = c_pinfo + (y & 2047u) + boff * 8;
+  ItemSigns sg;
+  sg.tslot = sT32 + __byte_perm(slots4, 0u, ((y >> 19) & 3u) | 0x4440u) * 16u;
+  const unsigned y1 = y << 1, y2 = y << 2;  // sy, sx at bit 31
+  sg.mc = y & 0x80000000u;
+  sg.mxy = (y1 ^ y2) & 0x80000000u;
+  sg.mxz = (y ^ y2) & 0x80000000u;
+  sg.myz = (y ^ y1) & 0x80000000u;
+  sg.mxyc = sg.mxy ^ sg.mc;
+  sg.mxzc = sg.mxz ^ sg.mc;
+  sg.myzc = sg.myz ^ sg.mc;
+#if KF_BPAIR == 0
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+    if ((vm >> b) & 1u) sparse_block<KML>(acc[b], U, sg.tslot + (inf[b * 8] & 63u) * OB, sg);
+  return;
+#endif
 #pragma unroll
   for (int b = 0; b < NB; b += 2) {
     const unsigned two = (vm >> b) & 3u;
     if (two == 3u) {
-      const unsigned t0 = tslot + (inf[b * 8] & 63u) * OB, t1 = tslot + (inf[(b + 1) * 8] & 63u) * OB;
-      sparse_block_s<KML, SP>(acc[b], U, t0);
-      sparse_block_s<KML, SP>(acc[b + 1], U, t1);
+      const unsigned t0 = sg.tslot + (inf[b * 8] & 63u) * OB, t1 = sg.tslot + (inf[(b + 1) * 8] & 63u) * OB;
+      sparse_block<KML>(acc[b], U, t0, sg);
+      sparse_block<KML>(acc[b + 1], U, t1, sg);
     } else if (two == 1u) {
-      sparse_block_s<KML, SP>(acc[b], U, tslot + (inf[b * 8] & 63u) * OB);
+      sparse_block<KML>(acc[b], U, sg.tslot + (inf[b * 8] & 63u) * OB, sg);
     } else if (two == 2u) {
-      sparse_block_s<KML, SP>(acc[b + 1], U, tslot + (inf[(b + 1) * 8] & 63u) * OB);
+      sparse_block<KML>(acc[b + 1], U, sg.tslot + (inf[(b + 1) * 8] & 63u) * OB, sg);
     }
-  }
-}
-
-template <int KML, int NB>
-__device__ __forceinline__ void sparse_apply(double2 (&acc)[NB][KML], const double2 (&U)[KML], int2 it,
-                                             unsigned sT32, int rs, int boff) {
-  const int dd = it.y & 31, c = (it.y >> 5) & 7;
-  const unsigned vm = ((unsigned)it.y >> 8) & 255u, sp = ((unsigned)it.y >> 16) & 7u;
-  const uint16_t* inf = c_pinfo + dd * 64 + boff * 8 + c;
-  // reflection of the item: fx iff sx != sz, fy iff sy != sz
-  const unsigned r = ((sp ^ (sp >> 2)) & 1u) | ((((sp >> 1) ^ (sp >> 2)) & 1u) << 1);
-  const unsigned tslot = sT32 + (unsigned)(((rs >> (5 * r)) & 31) * 16);
-  switch (KML == 1 ? (sp & 4u) : sp) {
-    case 0: sparse_item_s<KML, NB, 0>(acc, U, vm, inf, tslot); break;
-    case 1: sparse_item_s<KML, NB, 1>(acc, U, vm, inf, tslot); break;
-    case 2: sparse_item_s<KML, NB, 2>(acc, U, vm, inf, tslot); break;
-    case 3: sparse_item_s<KML, NB, 3>(acc, U, vm, inf, tslot); break;
-    case 4: sparse_item_s<KML, NB, 4>(acc, U, vm, inf, tslot); break;
-    case 5: sparse_item_s<KML, NB, 5>(acc, U, vm, inf, tslot); break;
-    case 6: sparse_item_s<KML, NB, 6>(acc, U, vm, inf, tslot); break;
-    default: sparse_item_s<KML, NB, 7>(acc, U, vm, inf, tslot); break;
   }
 }
 
@@ -727,9 +741,12 @@ constexpr int ITEM_PF = KF_ITEM_PF;  // items ahead whose source spectra are pre
 // NB = 4: a half parent (children 4h .. 4h + 3, h = the x bit of the octant; ord carries
 // 2P + h), half the accumulators, 16 warps per SM -- the source spectra of an item are
 // loaded once per half
+#ifndef KF_ITEM_WARPS4
+#define KF_ITEM_WARPS4 16
+#endif
 template <int NB>
 struct ItemCfg {
-  static constexpr int WARPS = NB == 8 ? SP_WARPS : 16;
+  static constexpr int WARPS = NB == 8 ? SP_WARPS : KF_ITEM_WARPS4;
 };
 
 template <int KML, int NB>
@@ -750,8 +767,12 @@ __global__ void __launch_bounds__(ItemCfg<NB>::WARPS * 32, 1)
   unsigned sT32;  // produced after the barrier (volatile), so no table read moves above it
   asm volatile("mov.u32 %0, %1;" : "=r"(sT32) : "r"((unsigned)__cvta_generic_to_shared(sTb)));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rs = rslot[g * 32 + lane];
-  const double2* ubg = ub + (int64_t)g * nq * R * 32;
+  unsigned slots4;  // the lane's bin slot under the 4 reflections, one byte each
+  {
+    const int rs = rslot[g * 32 + lane];
+    slots4 = (rs & 31) | (((rs >> 5) & 31) << 8) | (((rs >> 10) & 31) << 16) | (((rs >> 15) & 31) << 24);
+  }
+  const double2* ubg = ub + (int64_t)g * nq * R * 32 + lane;
   // the warp's parents: positions [wrange[r], wrange[r + 1]) of the processing order ord
   // (setup deals the chunk's parents round-robin to the nrange warps of a frequency group,
   // so at any time the running warps share a window of Morton-adjacent parents and the
@@ -770,23 +791,12 @@ __global__ void __launch_bounds__(ItemCfg<NB>::WARPS * 32, 1)
   int pid = pb + lane < pe ? ord[pb + lane] : 0;
   unsigned ppat = pb + lane < pe ? unit_pat(pid) : 0u;
   const int ibeg = ioff[pa], iend = ioff[pe];
-  // item batches: lane l holds items[ib + l] (bat) and items[ib + 32 + l] (batn)
+  // item batches: lane l holds items[ib + l] (bat) and items[ib + 32 + l] (batn); an item
+  // is {x = offset of its source spectra block (KML rows of 32 bins) from the group base,
+  // y = item word (sparse_apply)}
   int ib = ibeg;
   int2 bat = ib + lane < iend ? items[ib + lane] : make_int2(0, 0);
   int2 batn = ib + 32 + lane < iend ? items[ib + 32 + lane] : make_int2(0, 0);
-  auto item_at = [&](int j) {  // j in [ib, ib + 64), warp-uniform
-    const int k = j - ib;
-    const int2 src = k < 32 ? bat : batn;
-    return make_int2(__shfl_sync(0xffffffffu, src.x, k & 31), __shfl_sync(0xffffffffu, src.y, k & 31));
-  };
-  // the 3 rows of source child c of parent q: one contiguous run of KML x 32 x 16 B
-  auto ublock = [&](int2 t) { return ubg + ((int64_t)t.x * R + ((t.y >> 5) & 7) * KML) * 32; };
-  auto prefetch = [&](int j) {
-    if (j < iend) {
-      const double2* u = ublock(item_at(j));
-      if (lane < KML * 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(u + lane * 8));
-    }
-  };
   double2 acc[NB][KML];
 #pragma unroll
   for (int b = 0; b < NB; ++b)
@@ -822,40 +832,51 @@ __global__ void __launch_bounds__(ItemCfg<NB>::WARPS * 32, 1)
     }
   };
   if (NB == 4) boff = 4 * (__shfl_sync(0xffffffffu, pid, 0) & 1);
-  double2 U[KML];
-  int2 it = make_int2(0, 0);
-  if (ibeg < iend) {
-    for (int j = ibeg + 1; j <= ibeg + ITEM_PF; ++j) prefetch(j);
-    it = item_at(ibeg);
-    const double2* uq = ublock(it) + lane;
+  // item j's field (x or y), j in [ib, ib + 64), warp-uniform
+  auto field = [&](int j, bool wantx) {
+    const int k = j - ib;
+    const int2 src = k < 32 ? bat : batn;
+    return __shfl_sync(0xffffffffu, wantx ? src.x : src.y, k & 31);
+  };
+  auto load_u = [&](int off, double2(&Ud)[KML]) {
 #pragma unroll
-    for (int e = 0; e < KML; ++e) U[e] = uq[e * 32];
-  }
-  for (int i = ibeg; i < iend; ++i) {
+    for (int e = 0; e < KML; ++e) Ud[e] = ubg[off + e * 32];
+  };
+  // one item: refill the batch window, pull the spectra ITEM_PF items ahead into L2, load
+  // the next item's spectra into Un (in flight during this item's products), apply
+  auto step = [&](int i, double2(&Uc)[KML], double2(&Un)[KML], unsigned& yc) {
     while (i == pcur_end) flush();  // parents ending here (also those without items)
-    // next item and its source spectra, in flight during this item's products; the
-    // spectra ITEM_PF items ahead are pulled into L2
     const int j = i + 1;
     if (j - ib == 32) {
       ib = j;
       bat = batn;
       batn = ib + 32 + lane < iend ? items[ib + 32 + lane] : make_int2(0, 0);
     }
-    prefetch(i + ITEM_PF);
-    int2 nx = it;
-    double2 Un[KML];
-#pragma unroll
-    for (int e = 0; e < KML; ++e) Un[e] = U[e];
-    if (j < iend) {
-      nx = item_at(j);
-      const double2* uq = ublock(nx) + lane;
-#pragma unroll
-      for (int e = 0; e < KML; ++e) Un[e] = uq[e * 32];
+    if (i + ITEM_PF < iend) {
+      const int off = field(i + ITEM_PF, true);
+      if (lane < KML * 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(ubg - lane + off + lane * 8));
     }
-    sparse_apply<KML, NB>(acc, U, it, sT32, rs, boff);
-    it = nx;
-#pragma unroll
-    for (int e = 0; e < KML; ++e) U[e] = Un[e];
+    unsigned yn = 0;
+    if (j < iend) {
+      load_u(field(j, true), Un);
+      yn = (unsigned)field(j, false);
+    }
+    sparse_apply<KML, NB>(acc, Uc, yc, sT32, slots4, boff);
+    yc = yn;
+  };
+  double2 U0[KML], U1[KML];
+  unsigned y = 0;
+  if (ibeg < iend) {
+    for (int j = ibeg + 1; j <= ibeg + ITEM_PF && j < iend; ++j) {
+      const int off = field(j, true);
+      if (lane < KML * 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(ubg - lane + off + lane * 8));
+    }
+    load_u(field(ibeg, true), U0);
+    y = (unsigned)field(ibeg, false);
+  }
+  for (int i = ibeg; i < iend; i += 2) {  // two items per trip: the spectra registers alternate
+    step(i, U0, U1, y);
+    if (i + 1 < iend) step(i + 1, U1, U0, y);
   }
   while (P < pe) flush();
 }
@@ -954,10 +975,11 @@ bool fft_supported_p(int p) { return (p >= 3 && p <= 8) || p == 10 || p == 12; }
 #endif
 constexpr int NT_L = KF_NT_L, NT_G = KF_NT_G;  // parent n-tiles per warp (Laplace, Stokes family); measured best (profiles/)
 
-// target children per warp unit of the sparse product: 8 (whole parent) or 4 (half parent);
+// target children per warp unit of the sparse product: 4 (half parent, 16 warps per SM;
+// C5 product 544 ms against 614 ms for whole parents with paired blocks, gpurun_out r02 l);
 // KAFMM_ITEM_NB=4|8 overrides (tuning knob, read at plan setup and launch)
 int item_nb() {
-  static const int v = getenv("KAFMM_ITEM_NB") ? (atoi(getenv("KAFMM_ITEM_NB")) == 4 ? 4 : 8) : 8;
+  static const int v = getenv("KAFMM_ITEM_NB") ? (atoi(getenv("KAFMM_ITEM_NB")) == 8 ? 8 : 4) : 4;
   return v;
 }
 
@@ -1200,6 +1222,7 @@ void build_fft_m2l(Plan& P, int64_t budget) {
             int v = -1;
             if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) >= 2)
               v = tab[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)] * NC + (kml == 1 ? 0 : sym[a][e]);
+            if (v >= 0) v = kml == 1 ? SPOS1[v] : SPOS3[v];  // shared-memory position (kafmm_spos.h)
             ai[((size_t)(dd * KS + ks) * kml + m) * 32 + lane] = (int16_t)v;
           }
     }
@@ -1474,7 +1497,11 @@ void build_fft_chunks(Plan& P, int64_t budget) {
                   const int ck = (c >> (2 - k)) & 1;
                   if (dv[k] < 0 || (dv[k] == 0 && ck == 0)) sp |= 1 << k;
                 }
-                all.push_back(make_int2(qq, dd | (c << 5) | (int)(vm << 8) | (sp << 16)));
+                const int r = ((sp & 1) ^ (sp >> 2)) | ((((sp >> 1) & 1) ^ (sp >> 2)) << 1);
+                const int64_t off = ((int64_t)qq * R + c * P.kml) * 32;
+                if (off >= INT32_MAX) throw Error{KAFMM_EINVAL, "FFT M2L chunk too large for the item stream"};
+                all.push_back(make_int2((int)off, (int)((unsigned)(dd * 64 + c) | (vm << 11) | ((unsigned)r << 19) |
+                                                        ((unsigned)sp << 29))));
                 ++cnt[q];
               }
             }
@@ -1504,9 +1531,9 @@ void build_fft_chunks(Plan& P, int64_t budget) {
             for (int64_t e = start[q]; e < start[q + 1]; ++e) {
               int2 it = all[e];
               if (halves == 2) {
-                const unsigned vm = (((unsigned)it.y >> 8) >> (4 * h)) & 15u;
+                const unsigned vm = (((unsigned)it.y >> 11) >> (4 * h)) & 15u;
                 if (!vm) continue;
-                it.y = (it.y & ~0xFF00) | (int)(vm << 8);
+                it.y = (int)(((unsigned)it.y & ~(255u << 11)) | (vm << 11));
               }
               items.push_back(it);
             }

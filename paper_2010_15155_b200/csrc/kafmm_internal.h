@@ -185,6 +185,10 @@ struct Plan {
   cudaStream_t stream = 0;
   cudaStream_t side = nullptr;         // near field (P2P) overlapped with the far-field chain
   cudaEvent_t ev_near_in = nullptr, ev_near_out = nullptr;
+  // multi-GPU: the E2 / E3 exchanges run on cstream while the plan's stream runs S2L
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_up = nullptr, ev_ghost = nullptr;
+  bool s2l_early = false;              // S2L already issued for this evaluation (before M2L)
   bool near_async = false;             // P2P of the current eval runs on `side`
   // CUDA graph of one evaluation (kafmm_set_graph): captured on `cap` for a
   // given (src, out, M2L mode) and replayed; the caller's stream is joined by events
@@ -377,7 +381,8 @@ void build_gemm_batches(Plan& P);                            // kafmm_tree.cu
 void upload_batch(Plan& P, GemmBatch& g, const std::vector<int2>& h_items);
 void run_eval(Plan& P, const double* d_src, double* d_out);  // kafmm_eval.cu
 void run_eval_up(Plan& P, const double* d_src);               // a1-a4
-void run_eval_down(Plan& P, double* d_out);                   // a5-a12
+void run_eval_down(Plan& P, double* d_out);
+void run_eval_s2l(Plan& P);  // CHK reset + S2L ahead of M2L (multi-GPU overlap); run_eval_down then skips them                   // a5-a12
 void build_m2l_batch(Plan& P);                                // kafmm_dist.cu
 void setup_dist(Plan& P, const double* d_local_points, int64_t n_local);  // kafmm_dist.cu (P.dist->comm set)
 void run_eval_dist(Plan& P, const double* d_local_src, double* d_local_out);

@@ -3,7 +3,7 @@ the M2L product kernels: per-launch ms / GB and the totals.  Usage: prod_launche
 import csv
 import sys
 
-SCALE = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+SCALE = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3,
          "byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0}
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 h, data = rows[0], rows[1:]
