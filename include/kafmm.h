@@ -201,10 +201,11 @@ const char* kafmm_stage_name(int stage);
 kafmm_status kafmm_set_m2l_mode(kafmm_plan plan, int mode);
 kafmm_status kafmm_get_m2l_mode(kafmm_plan plan, int* mode);
 
-/* FFT M2L work summary, st[8]: chunks, source parent blocks (incl. halos
+/* FFT M2L work summary, st[10]: chunks, source parent blocks (incl. halos
  * transformed once per chunk), target parents, target boxes, V pairs, chunks
  * whose product runs per pair under the current mode, frequency bins NF,
- * spectra budget in bytes. */
+ * spectra budget in bytes, existing source children (transforms per component),
+ * items of the sparse-chunk product stream. */
 kafmm_status kafmm_fft_stats(kafmm_plan plan, int64_t* st);
 
 /* CUDA graph replay of kafmm_eval (on = 1): the first evaluation with a given

@@ -640,9 +640,11 @@ kafmm_status kafmm_get_m2l_mode(kafmm_plan plan, int* mode) {
 
 kafmm_status kafmm_fft_stats(kafmm_plan plan, int64_t* st) {
   if (!plan || !st) return KAFMM_EINVAL;
-  for (int i = 0; i < 8; ++i) st[i] = 0;
+  for (int i = 0; i < 10; ++i) st[i] = 0;
   for (const FftChunk& ch : plan->fft_chunks) {
     st[0] += 1;
+    st[8] += ch.nsrc_children;
+    st[9] += ch.nitems;
     st[1] += ch.nq;
     st[2] += ch.npar;
     st[3] += ch.nt;

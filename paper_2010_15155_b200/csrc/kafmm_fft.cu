@@ -252,7 +252,7 @@ __device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* 
       },
       [&](int L, int o, double2 v) {
         const int r = L / NBC, t = L - r * NBC, f = o * NGNZ + r, sl = pick<NB>(slot, t, NBC);
-        if (fpos) {  // sparse chunks: [group][q][R][slot] (k_m2l_sparse)
+        if (fpos) {  // sparse chunks: [group][q][R][slot] (k_m2l_items)
           const int fp = __ldg(fpos + f);
           ub[(((int64_t)(fp >> 5) * nq + q) * R + sl) * 32 + (fp & 31)] = v;
         } else
@@ -526,103 +526,8 @@ __device__ __forceinline__ double xsign(double v, unsigned m) {  // flip the sig
   return __hiloint2double(__double2hiint(v) ^ (int)m, __double2loint(v));
 }
 
-template <int KML>
-__global__ void __launch_bounds__(SP_WARPS * 32, 1)
-    k_m2l_sparse(int64_t npar, int64_t nq, int NFP, const double2* __restrict__ tbase, const int* __restrict__ rslot,
-                 const double2* __restrict__ ub, double2* __restrict__ cb, const int32_t* __restrict__ nbr,
-                 const uint8_t* __restrict__ tpat, const uint8_t* __restrict__ qpat) {
-  constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
-  extern __shared__ __align__(16) double2 sTb[];  // [N_BASE][NC][32]
-  const int g = blockIdx.y;
-  {
-    const double4* src = reinterpret_cast<const double4*>(tbase + (int64_t)g * N_BASE * NC * 32);
-    double4* dst = reinterpret_cast<double4*>(sTb);
-    for (int i = threadIdx.x; i < N_BASE * NC * 16; i += SP_WARPS * 32) dst[i] = src[i];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rs = rslot[g * 32 + lane];
-  const double2* ubg = ub + (int64_t)g * nq * R * 32 + lane;
-  for (int64_t P = (int64_t)blockIdx.x * SP_WARPS + warp; P < npar; P += (int64_t)gridDim.x * SP_WARPS) {
-    const unsigned bm = tpat[P];
-    if (!bm) continue;
-    double2 acc[8][KML];
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-#pragma unroll
-      for (int a = 0; a < KML; ++a) acc[b][a] = make_double2(0.0, 0.0);
-    for (int d = 0; d < 26; ++d) {
-      const int q = nbr[P * 26 + d];
-      if (q < 0) continue;
-      unsigned cm = qpat[q];
-      if (!cm) continue;
-      const double2* uq = ubg + (int64_t)q * R * 32;
-      const uint16_t* inf = c_pinfo + d * 64;
-      int c = __ffs(cm) - 1;
-      double2 U[KML];
-#pragma unroll
-      for (int e = 0; e < KML; ++e) U[e] = uq[(c * KML + e) * 32];
-      while (true) {
-        cm &= cm - 1;
-        const int cn = cm ? __ffs(cm) - 1 : -1;
-        double2 Un[KML];
-        if (cn >= 0) {  // next source child's spectra in flight during this one's products
-#pragma unroll
-          for (int e = 0; e < KML; ++e) Un[e] = uq[(cn * KML + e) * 32];
-        }
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          if (!((bm >> b) & 1u)) continue;
-          const unsigned info = inf[b * 8 + c];
-          if (info == 0xFFFFu) continue;
-          const int slot = (rs >> (5 * ((info >> 6) & 3))) & 31;
-          const double2* t = sTb + (info & 63) * NC * 32 + slot;
-          const unsigned mc = ((info >> 8) & 1u) << 31;  // conj: flip imaginary parts
-          if (KML == 1) {
-            const double2 t0 = t[0];
-            cmac(acc[b][0], make_double2(t0.x, xsign(t0.y, mc)), U[0]);
-          } else {
-            const unsigned mxy = ((info >> 9) & 1u) << 31, mxz = ((info >> 10) & 1u) << 31,
-                           myz = ((info >> 11) & 1u) << 31;
-            double2 T[6];
-#pragma unroll
-            for (int k = 0; k < 6; ++k) T[k] = t[k * 32];
-            T[0].y = xsign(T[0].y, mc);
-            T[3].y = xsign(T[3].y, mc);
-            T[5].y = xsign(T[5].y, mc);
-            T[1] = make_double2(xsign(T[1].x, mxy), xsign(T[1].y, mxy ^ mc));
-            T[2] = make_double2(xsign(T[2].x, mxz), xsign(T[2].y, mxz ^ mc));
-            T[4] = make_double2(xsign(T[4].x, myz), xsign(T[4].y, myz ^ mc));
-            double2* o = acc[b];
-            cmac(o[0], T[0], U[0]);
-            cmac(o[0], T[1], U[KML > 1 ? 1 : 0]);
-            cmac(o[0], T[2], U[KML > 2 ? 2 : 0]);
-            cmac(o[KML > 1 ? 1 : 0], T[1], U[0]);
-            cmac(o[KML > 1 ? 1 : 0], T[3], U[KML > 1 ? 1 : 0]);
-            cmac(o[KML > 1 ? 1 : 0], T[4], U[KML > 2 ? 2 : 0]);
-            cmac(o[KML > 2 ? 2 : 0], T[2], U[0]);
-            cmac(o[KML > 2 ? 2 : 0], T[4], U[KML > 1 ? 1 : 0]);
-            cmac(o[KML > 2 ? 2 : 0], T[5], U[KML > 2 ? 2 : 0]);
-          }
-        }
-        if (cn < 0) break;
-        c = cn;
-#pragma unroll
-        for (int e = 0; e < KML; ++e) U[e] = Un[e];
-      }
-    }
-    double2* o = cb + (P * R) * (int64_t)NFP + g * 32 + lane;
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-      if ((bm >> b) & 1u) {
-#pragma unroll
-        for (int a = 0; a < KML; ++a) o[(int64_t)(b * KML + a) * NFP] = acc[b][a];
-      }
-  }
-}
-
 // The sparse-chunk product over a precomputed item stream (the default for sparse
-// chunks).  Same arithmetic and table as k_m2l_sparse; what changes is how a warp
+// chunks).  Same arithmetic and table as round 2's first sparse kernel; what changes is how a warp
 // finds its work.  Per chunk, setup lists for every target parent P its items
 // (d, c): a non-leaf colleague Q_d and an existing child c of it such that some
 // existing child b of P is a V-list target of c, with
@@ -632,10 +537,10 @@ __global__ void __launch_bounds__(SP_WARPS * 32, 1)
 // items and parent boundaries arrive 32 at a time (one coalesced load per lane,
 // broadcast by shuffles, the next batch in flight), and the source spectra of the
 // next item are loaded while the current one is applied, so no global load sits
-// between two items' multiply-adds (k_m2l_sparse walked the 26 directions with a
+// between two items' multiply-adds (that kernel walked the 26 directions with a
 // dependent nbr -> qpat -> ub load chain per direction: 2/3 of them empty on the
 // C5 sphere cloud, and long-scoreboard stalls were 1/3 of its samples,
-// profiles/r02_C5_sparse_ncu.txt).
+// profiles/r02_C5_product_ncu.txt).
 // 16-B shared-memory load through a 32-bit shared address (the generic-pointer form
 // re-derived the CTA's shared window -- S2UR SR_CgaCtaId, an XU-pipe op -- in front of
 // every b block; the XU pipe then ran at 3.5x its sustained rate in ncu)
@@ -654,7 +559,7 @@ __device__ __forceinline__ double2 lds_f64x2(unsigned a) {
 // stores S in bits 16-18 of the item word, the masks are formed once per item, and a
 // block costs the base-offset lookup, six table loads and the sign flips.  (One code
 // variant per sign pattern, with the flips folded into the multiply-adds, overflowed
-// the instruction cache: 2.4x slower, profiles/r02_C5_items_ncu.txt.)
+// the instruction cache: 2.4x slower, profiles/r02_C5_product_ncu.txt.)
 struct ItemSigns {
   unsigned tslot;                            // shared address of the item's reflected bin slot
   unsigned mc, mxy, mxyc, mxz, mxzc, myz, myzc;  // sign-bit masks (bit 31)
@@ -976,7 +881,7 @@ bool fft_supported_p(int p) { return (p >= 3 && p <= 8) || p == 10 || p == 12; }
 constexpr int NT_L = KF_NT_L, NT_G = KF_NT_G;  // parent n-tiles per warp (Laplace, Stokes family); measured best (profiles/)
 
 // target children per warp unit of the sparse product: 4 (half parent, 16 warps per SM;
-// C5 product 544 ms against 614 ms for whole parents with paired blocks, gpurun_out r02 l);
+// C5 product 544 ms against 614 ms for whole parents with paired blocks, profiles/r02_C5_product_ab.txt);
 // KAFMM_ITEM_NB=4|8 overrides (tuning knob, read at plan setup and launch)
 int item_nb() {
   static const int v = getenv("KAFMM_ITEM_NB") ? (atoi(getenv("KAFMM_ITEM_NB")) == 8 ? 8 : 4) : 4;
@@ -990,20 +895,11 @@ void run_m2l_fft(Plan& Pl) {
     const bool pairs = chunk_uses_pairs(Pl, ch);
     prod_mark(Pl);
     if (pairs) {
-      // warp per target parent, 32 bins per CTA (group), parents strided over the CTAs
-      // of a group; the grid's x extent keeps every CTA on >= 16 parents per warp so the
-      // 172 KB table stage is amortised
+      // k_m2l_items: grid (CTAs per frequency group, groups); one CTA per SM (the 172 KB
+      // operator table of its 32 bins), each warp a run of units of the item stream
       const int NC = Pl.kml == 1 ? 1 : 6;
       const size_t smem = (size_t)N_BASE * NC * 32 * sizeof(double2);
-      static std::atomic<uint64_t> attr{0};
-      if (first_on_device(attr)) {
-        KF_CUDA(cudaFuncSetAttribute(k_m2l_sparse<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(N_BASE * 32 * sizeof(double2))));
-        KF_CUDA(cudaFuncSetAttribute(k_m2l_sparse<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(N_BASE * 6 * 32 * sizeof(double2))));
-      }
-      static const bool dirs = getenv("KAFMM_SPARSE_DIRS") != nullptr;  // A/B knob: the direction walk
-      if (!dirs) {
+      {
         static std::atomic<uint64_t> attr2{0};
         if (first_on_device(attr2)) {
           for (auto fn : {k_m2l_items<1, 8>, k_m2l_items<1, 4>})
@@ -1028,15 +924,6 @@ void run_m2l_fft(Plan& Pl) {
           else KF_ITEMS(3, 4);
         }
 #undef KF_ITEMS
-      } else {
-      const int64_t per_cta = (int64_t)SP_WARPS * 16;
-      const dim3 grid((unsigned)std::max<int64_t>(1, (ch.npar + per_cta - 1) / per_cta), (unsigned)Pl.NFG);
-      if (Pl.kml == 1)
-        k_m2l_sparse<1><<<grid, SP_WARPS * 32, smem, Pl.stream>>>(ch.npar, ch.nq, Pl.NFP, Pl.d_tbase, Pl.d_rslot,
-                                                                  Pl.d_ub, Pl.d_cb, ch.d_nbr, ch.d_tpat, ch.d_qpat);
-      else
-        k_m2l_sparse<3><<<grid, SP_WARPS * 32, smem, Pl.stream>>>(ch.npar, ch.nq, Pl.NFP, Pl.d_tbase, Pl.d_rslot,
-                                                                  Pl.d_ub, Pl.d_cb, ch.d_nbr, ch.d_tpat, ch.d_qpat);
       }
     } else {
       // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
@@ -1079,7 +966,7 @@ static void d2h(Plan& P, std::vector<T>& h, const T* d, int64_t n) {
 }
 
 // Frequency groups, positions and the reflected-offset tables of the sparse product
-// (k_m2l_sparse).  Orbits of a bin under (fx, fy) -> (+-fx, +-fy) have 4, 2 or 1
+// (k_m2l_items).  Orbits of a bin under (fx, fy) -> (+-fx, +-fy) have 4, 2 or 1
 // members; they are packed into 8-slot phases (never straddling one) and the phases
 // into groups of 32 slots.
 static void build_sparse_tables(Plan& P, const int16_t* tab) {
@@ -1363,7 +1250,7 @@ void build_fft_chunks(Plan& P, int64_t budget) {
   const int64_t per_block = (int64_t)R * P.NFP * 16;  // one parent block of spectra
   for (FftChunk& c : P.fft_chunks)  // re-planning (kafmm_restrict): release the old lists
     for (void* p : {(void*)c.d_qbox, (void*)c.d_nbr, (void*)c.d_tbox, (void*)c.d_tpb, (void*)c.d_toff,
-                    (void*)c.d_tpat, (void*)c.d_qpat, (void*)c.d_ioff, (void*)c.d_items, (void*)c.d_wrange,
+                    (void*)c.d_tpat, (void*)c.d_ioff, (void*)c.d_items, (void*)c.d_wrange,
                     (void*)c.d_ord})
       dfree(P, p);
   P.fft_chunks.clear();
@@ -1433,7 +1320,10 @@ void build_fft_chunks(Plan& P, int64_t budget) {
       for (int64_t q = 0; q < ch.nq; ++q)
         for (int o = 0; o < 8; ++o) {
           const int32_t c = child[8 * (int64_t)qs[q] + o];
-          if (c >= 0 && (P.h_row.empty() || P.h_row[c] >= 0)) qpat[q] |= (uint8_t)(1u << o);
+          if (c >= 0 && (P.h_row.empty() || P.h_row[c] >= 0)) {
+            qpat[q] |= (uint8_t)(1u << o);
+            ++ch.nsrc_children;
+          }
         }
       for (size_t ii = 0; ii < tb.size(); ++ii) {
         const int32_t t = tb[ii];
@@ -1555,9 +1445,7 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         KF_CUDA(cudaStreamSynchronize(st));
       }
       ch.d_tpat = dalloc<uint8_t>(P, std::max<int64_t>(1, ch.npar));
-      ch.d_qpat = dalloc<uint8_t>(P, std::max<int64_t>(1, ch.nq));
       KF_CUDA(cudaMemcpyAsync(ch.d_tpat, tpat.data(), ch.npar, cudaMemcpyHostToDevice, st));
-      if (ch.nq) KF_CUDA(cudaMemcpyAsync(ch.d_qpat, qpat.data(), ch.nq, cudaMemcpyHostToDevice, st));
       ch.d_qbox = dalloc<int32_t>(P, std::max<int64_t>(1, ch.nq));
       ch.d_nbr = dalloc<int32_t>(P, ch.npar * 26);
       ch.d_tbox = dalloc<int32_t>(P, std::max<int64_t>(1, ch.nt));

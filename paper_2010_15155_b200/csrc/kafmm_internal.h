@@ -71,18 +71,18 @@ struct FftChunk {
   int32_t* d_tbox = nullptr;  // nt target box ids
   int2* d_tpb = nullptr;      // nt: (local parent index, child octant)
   int32_t* d_toff = nullptr;  // npar + 1: targets of local parent P are [toff[P], toff[P+1])
-  // child occupancy for the sparse-chunk product (k_m2l_sparse): bit c of tpat[P] =
-  // target parent P's child c exists (and is active on this rank); qpat[q] the same
-  // for source parent q's children
+  // child occupancy for the sparse-chunk product (k_m2l_items): bit c of tpat[P] =
+  // target parent P's child c exists (and is active on this rank)
   int64_t npairs = 0;           // V pairs of the chunk
   uint8_t* d_tpat = nullptr;    // npar
-  uint8_t* d_qpat = nullptr;    // nq
-  // item stream of the sparse product (k_m2l_items): per target parent P the (colleague
-  // direction d, source child c) items with a non-empty target mask, CSR over parents
-  int32_t* d_ioff = nullptr;    // npar + 1, in processing order (d_ord)
-  int2* d_items = nullptr;      // {q, d | c << 5 | vmask << 8}
+  // item stream of the sparse product (k_m2l_items): per unit (target parent, or half of
+  // one) the (colleague direction d, source child c) items with a non-empty target mask,
+  // CSR over the units in processing order
+  int32_t* d_ioff = nullptr;    // units + 1
+  int2* d_items = nullptr;      // {spectra block offset, item word: d*64+c | vmask << 11 | r << 19 | S << 29}
   int64_t nitems = 0;
-  int32_t* d_ord = nullptr;     // npar: processing order of the parents (chunk-local ids)
+  int64_t nsrc_children = 0;    // existing children of the chunk's source parents
+  int32_t* d_ord = nullptr;     // units: processing order (parent id, or 2 parent + half)
   int32_t* d_wrange = nullptr;  // nrange + 1: each warp's positions in that order
   int64_t nrange = 0;
   double block_fill = 1.0;      // V pairs / (8x8 child blocks the DMMA product runs)

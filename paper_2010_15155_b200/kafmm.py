@@ -251,10 +251,10 @@ class KAFMM:
         _check(self.lib.kafmm_set_graph(self.h, int(bool(on))), "kafmm_set_graph")
 
     def fft_stats(self) -> dict:
-        st = np.zeros(8, np.int64)
+        st = np.zeros(10, np.int64)
         _check(self.lib.kafmm_fft_stats(self.h, C.c_void_p(st.ctypes.data)), "kafmm_fft_stats")
         keys = ("chunks", "source_blocks", "target_parents", "targets", "v_pairs", "pair_chunks", "n_freq",
-                "budget_bytes")
+                "budget_bytes", "source_children", "items")
         return {k: int(v) for k, v in zip(keys, st)}
 
     def launch_count(self) -> int:

@@ -1,4 +1,4 @@
-"""M2L offset symmetry used by the per-pair FFT product (k_m2l_sparse, which reads the spectra of the 56 offsets |o| and reflects them).
+"""M2L offset symmetry used by the per-pair FFT product (k_m2l_items, which reads the spectra of the 56 offsets |o| and reflects them).
 
 The product keeps the operator spectra of only the 158 offsets o of one half and
 reads offset -o as the conjugate.  In real space that is K_{-o} = K_o^T for the
