@@ -87,11 +87,29 @@ __global__ void k_spectra_transpose(int NF, int nc, const double2* __restrict__ 
 // ---------------------------------------------------------------------------
 // hot path kernels
 // ---------------------------------------------------------------------------
+// Padded row lengths (complex entries) of the shared-memory arrays of the DFT passes:
+// forward z output [x y][fz] (ZS), forward y output [x][fy][fz] (YS), extra doubles between
+// the transforms of one CTA (FPAD), inverse x output [x][fy][fz] (DS) and y output
+// [x][y][fz] (ES).  Chosen by scripts/fft_banks.py, which replays every fragment load and
+// store of the passes and counts shared-memory wavefronts; unpadded rows of NZ = p
+// entries (p = 8: 128 B) put a warp's lines or outputs in one bank group (ncu, C5: 62-67%
+// of the DFT passes' wavefronts were bank conflicts, profiles/r02_C5_dft_ncu.txt).
+template <int P>
+struct FftPad {  // {ZS, YS, FPAD, DS, ES}; NZ = P
+  static constexpr int T[8][5] = {{5, 6, 8, 9, 3},     {4, 6, 8, 6, 6},     {12, 6, 4, 6, 6},  {12, 6, 0, 6, 6},
+                                  {12, 10, 4, 10, 10}, {12, 10, 8, 10, 10}, {12, 10, 0, 10, 10},
+                                  {12, 14, 8, 14, 14}};
+  static constexpr int I = P <= 8 ? P - 3 : (P == 10 ? 6 : 7);
+  static constexpr int ZS = T[I][0], YS = T[I][1], FPAD = T[I][2], DS = T[I][3], ES = T[I][4];
+};
+
 template <int P>
 struct FftDims {
   static constexpr int NG = 2 * P - 1, NZ = NG / 2 + 1, NF = NG * NG * NZ;
-  // inverse: x-pass output [x][fy][fz] + y-pass output [x][y][fz] (complex) + twiddles
-  static constexpr size_t INV_SMEM = (size_t)2 * (P * NG * NZ + P * P * NZ + NG) * sizeof(double);
+  static_assert(FftPad<P>::ZS >= NZ && FftPad<P>::YS >= NZ && FftPad<P>::DS >= NZ && FftPad<P>::ES >= NZ, "pad");
+  // inverse: x-pass output [x][fy][fz] + y-pass output [x][y][fz] (complex, padded rows) + twiddles
+  static constexpr size_t INV_SMEM =
+      (size_t)2 * (P * NG * FftPad<P>::DS + P * P * FftPad<P>::ES + NG) * sizeof(double);
 };
 
 __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
@@ -198,7 +216,8 @@ __device__ __forceinline__ void dft_pass(int nlines, int nout, const double* __r
 template <int P>
 struct FwdCfg {
   using D = FftDims<P>;
-  static constexpr int PER = 2 * (P * P * D::NZ + P * D::NG * D::NZ);  // doubles per transform (z, y outputs)
+  // doubles per transform (z, y outputs, padded rows)
+  static constexpr int PER = 2 * (P * P * FftPad<P>::ZS + P * D::NG * FftPad<P>::YS) + FftPad<P>::FPAD;
   template <int NB>
   static constexpr size_t smem() { return (size_t)NB * PER * sizeof(double); }
 };
@@ -219,7 +238,8 @@ __device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* 
                                          const double* __restrict__ wf, const int16_t* __restrict__ fpos) {
   using D = FftDims<P>;
   using S = DftShape<P>;
-  constexpr int NG = D::NG, NZ = D::NZ, NGNZ = NG * NZ, PER = FwdCfg<P>::PER, PP = P * P, YO = 2 * PP * NZ;
+  constexpr int NG = D::NG, NZ = D::NZ, NGNZ = NG * NZ, PER = FwdCfg<P>::PER, PP = P * P;
+  constexpr int ZS = FftPad<P>::ZS, YS = FftPad<P>::YS, YO = 2 * PP * ZS;
   dft_pass<S::KZ, S::NZT>(  // z: lines (t; x, y), real input from UE
       PP * NBC, NZ, wz,
       [&](int L, int k) {
@@ -230,25 +250,25 @@ __device__ __forceinline__ void fwd_body(double* __restrict__ sm, const double* 
       },
       [&](int L, int o, double2 v) {
         const int t = L / PP, xy = L - t * PP;
-        reinterpret_cast<double2*>(sm + t * PER)[xy * NZ + o] = v;
+        reinterpret_cast<double2*>(sm + t * PER)[xy * ZS + o] = v;
       });
   __syncthreads();
   dft_pass<S::KF, S::NFT>(  // y: lines (t; x, fz)
       P * NZ * NBC, NG, wf,
       [&](int L, int k) {
         const int t = L / (P * NZ), r = L - t * (P * NZ), x = r / NZ, fz = r - x * NZ, y = k >> 1;
-        return y < P ? sm[t * PER + 2 * ((x * P + y) * NZ + fz) + (k & 1)] : 0.0;
+        return y < P ? sm[t * PER + 2 * ((x * P + y) * ZS + fz) + (k & 1)] : 0.0;
       },
       [&](int L, int o, double2 v) {
         const int t = L / (P * NZ), r = L - t * (P * NZ), x = r / NZ, fz = r - x * NZ;
-        reinterpret_cast<double2*>(sm + t * PER + YO)[(x * NG + o) * NZ + fz] = v;
+        reinterpret_cast<double2*>(sm + t * PER + YO)[(x * NG + o) * YS + fz] = v;
       });
   __syncthreads();
   dft_pass<S::KF, S::NFT>(  // x: lines (fy, fz; t) -> global, frequency major
       NGNZ * NBC, NG, wf,
       [&](int L, int k) {
-        const int r = L / NBC, t = L - r * NBC, x = k >> 1;
-        return x < P ? sm[t * PER + YO + 2 * (x * NGNZ + r) + (k & 1)] : 0.0;
+        const int r = L / NBC, t = L - r * NBC, x = k >> 1, fy = r / NZ, fz = r - fy * NZ;
+        return x < P ? sm[t * PER + YO + 2 * ((x * NG + fy) * YS + fz) + (k & 1)] : 0.0;
       },
       [&](int L, int o, double2 v) {
         const int r = L / NBC, t = L - r * NBC, f = o * NGNZ + r, sl = pick<NB>(slot, t, NBC);
@@ -327,9 +347,10 @@ __global__ void __launch_bounds__(256)
   using S = DftShape<P>;
   constexpr int NG = D::NG, NZ = D::NZ, NGNZ = NG * NZ;
   extern __shared__ __align__(16) double sm[];
-  double2* Dx = reinterpret_cast<double2*>(sm);  // [x][fy][fz]
-  double2* E = Dx + P * NG * NZ;                 // [x][y][fz]
-  double2* tw = E + P * P * NZ;                  // exp(+2 pi i j / NG)
+  constexpr int DS = FftPad<P>::DS, ES = FftPad<P>::ES;
+  double2* Dx = reinterpret_cast<double2*>(sm);  // [x][fy][fz], rows of DS
+  double2* E = Dx + P * NG * DS;                 // [x][y][fz], rows of ES
+  double2* tw = E + P * P * ES;                  // exp(+2 pi i j / NG)
   const double* Dd = reinterpret_cast<const double*>(Dx);
   const int t = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
   const int64_t box = tbox[t];
@@ -351,23 +372,26 @@ __global__ void __launch_bounds__(256)
           const int fx = k >> 1;
           return fx < NG ? __ldg(col + 2 * __ldg(fpos + fx * NGNZ + line) + (k & 1)) : 0.0;
         },
-        [&](int line, int o, double2 v) { Dx[o * NGNZ + line] = v; });
+        [&](int line, int o, double2 v) {
+          const int fy = line / NZ, fz = line - fy * NZ;
+          Dx[(o * NG + fy) * DS + fz] = v;
+        });
     __syncthreads();
     dft_pass<S::KI, S::NIT>(  // y: lines (x, fz), outputs y < P
         P * NZ, P, wi,
         [&](int line, int k) {
           const int x = line / NZ, fz = line - x * NZ, fy = k >> 1;
-          return fy < NG ? Dd[2 * ((x * NG + fy) * NZ + fz) + (k & 1)] : 0.0;
+          return fy < NG ? Dd[2 * ((x * NG + fy) * DS + fz) + (k & 1)] : 0.0;
         },
         [&](int line, int o, double2 v) {
           const int x = line / NZ, fz = line - x * NZ;
-          E[(x * P + o) * NZ + fz] = v;
+          E[(x * P + o) * ES + fz] = v;
         });
     __syncthreads();
     double* o = chk + box * ldn;
     for (int m = tid; m < M; m += bd) {  // z: half spectrum -> real, only at surface points
       int x = lat[3 * m], y = lat[3 * m + 1], z = lat[3 * m + 2];
-      const double2* e = E + (x * P + y) * NZ;
+      const double2* e = E + (x * P + y) * ES;
       double v = 0.0;
       int k = z;
       for (int fz = 1; fz < NZ; ++fz) {
