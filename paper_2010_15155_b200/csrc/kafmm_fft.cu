@@ -810,6 +810,273 @@ __global__ void __launch_bounds__(ItemCfg<NB>::WARPS * 32, 1)
   while (P < pe) flush();
 }
 
+// ---------------------------------------------------------------------------
+// Sparse-chunk product with operator reuse (k_m2l_groups, the default for sparse chunks).
+// k_m2l_items loads one operator T_o(f) (6 x 16 B per lane) per V pair: six LDS.128 for
+// 36 DFMA, i.e. 24 shared-memory wavefronts per 18 FP64-pipe cycles -- the table, not the
+// FP64 pipe, bounds it.  But the offset o = 2d + c - b of a child pair depends only on
+// c - b within one colleague: in a half-parent unit (target children b = 4h + t, t =
+// (ty, tz)) and one x half cx of colleague Q_d (source children c = 4cx + c', c' = (cy, cz)),
+// the 16 pairs (t, c') share 9 offsets, indexed by (cy - ty, cz - tz).  A group =
+// (unit, d, cx) with its 16-bit pair mask: the lane holds the 4 source spectra and the
+// 4 accumulators, and each offset's T is loaded once for all the valid pairs that use
+// it (full 4 x 4 blocks: 9 loads per 16 pairs).  Group word y: bits 0-4 the direction
+// slot dd, bit 5 cx, bits 6-21 the pair mask (bit 4t + c'), bits 22-25 the source mask.
+// Signs and reflection per offset come from c_pinfo (S [conj] T_|o|(R f) S).
+template <int KML>
+__device__ __forceinline__ void load_T(double2 (&T)[KML == 1 ? 1 : 6], unsigned info, unsigned sT32,
+                                       unsigned slots4) {
+  constexpr unsigned OB = (KML == 1 ? 1 : 6) * 32 * 16;
+  const unsigned t = sT32 + __byte_perm(slots4, 0u, ((info >> 6) & 3u) | 0x4440u) * 16u + (info & 63u) * OB;
+  const unsigned mc = (info << 23) & 0x80000000u;
+  if (KML == 1) {
+    T[0] = lds_f64x2(t);
+    T[0].y = xsign(T[0].y, mc);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) T[k] = lds_f64x2(t + k * 32 * 16);
+    const unsigned mxy = (info << 22) & 0x80000000u, mxz = (info << 21) & 0x80000000u,
+                   myz = (info << 20) & 0x80000000u;
+    T[0].y = xsign(T[0].y, mc);
+    T[3].y = xsign(T[3].y, mc);
+    T[5].y = xsign(T[5].y, mc);
+    T[1] = make_double2(xsign(T[1].x, mxy), xsign(T[1].y, mxy ^ mc));
+    T[2] = make_double2(xsign(T[2].x, mxz), xsign(T[2].y, mxz ^ mc));
+    T[4] = make_double2(xsign(T[4].x, myz), xsign(T[4].y, myz ^ mc));
+  }
+}
+
+template <int KML>
+__device__ __forceinline__ void apply_T(double2 (&o)[KML], const double2 (&T)[KML == 1 ? 1 : 6],
+                                        const double2 (&U)[KML]) {
+  if (KML == 1) {
+    cmac(o[0], T[0], U[0]);
+  } else {
+    cmac(o[0], T[0], U[0]);
+    cmac(o[0], T[1], U[KML > 1 ? 1 : 0]);
+    cmac(o[0], T[2], U[KML > 2 ? 2 : 0]);
+    cmac(o[KML > 1 ? 1 : 0], T[1], U[0]);
+    cmac(o[KML > 1 ? 1 : 0], T[3], U[KML > 1 ? 1 : 0]);
+    cmac(o[KML > 1 ? 1 : 0], T[4], U[KML > 2 ? 2 : 0]);
+    cmac(o[KML > 2 ? 2 : 0], T[2], U[0]);
+    cmac(o[KML > 2 ? 2 : 0], T[4], U[KML > 1 ? 1 : 0]);
+    cmac(o[KML > 2 ? 2 : 0], T[5], U[KML > 2 ? 2 : 0]);
+  }
+}
+
+// pairs (t, c') of one offset delta = (cy - ty, cz - tz), DY, DZ in {-1, 0, 1}
+template <int DY, int DZ>
+struct GDelta {
+  static constexpr int cp(int t) { return 2 * (((t >> 1) & 1) + DY) + ((t & 1) + DZ); }
+  static constexpr bool ok(int t) {
+    return ((t >> 1) & 1) + DY >= 0 && ((t >> 1) & 1) + DY <= 1 && (t & 1) + DZ >= 0 && (t & 1) + DZ <= 1;
+  }
+  static constexpr unsigned mask() {
+    return (ok(0) ? 1u << cp(0) : 0u) | (ok(1) ? 1u << (4 + cp(1)) : 0u) | (ok(2) ? 1u << (8 + cp(2)) : 0u) |
+           (ok(3) ? 1u << (12 + cp(3)) : 0u);
+  }
+  static constexpr int t0() { return ok(0) ? 0 : ok(1) ? 1 : ok(2) ? 2 : 3; }
+};
+
+#ifndef KF_TSPLIT
+#define KF_TSPLIT 1
+#endif
+template <int KML, int DY, int DZ>
+__device__ __forceinline__ void group_delta(double2 (&acc)[4][KML], const double2 (&U)[4][KML], unsigned pm,
+                                            const uint16_t* inf, unsigned sT32, unsigned slots4) {
+  using D = GDelta<DY, DZ>;
+  if (!(pm & D::mask())) return;
+  const unsigned info = inf[D::t0() * 8 + D::cp(D::t0())];
+  if (KML == 3 && KF_TSPLIT) {
+    // the operator in two halves (T0..T2, then T3..T5): 12 registers live instead of 24,
+    // so 4 sources + 4 accumulators + T fit 128 registers (16 warps per SM)
+    constexpr unsigned OB = 6 * 32 * 16;
+    const unsigned ta = sT32 + __byte_perm(slots4, 0u, ((info >> 6) & 3u) | 0x4440u) * 16u + (info & 63u) * OB;
+    const unsigned mc = (info << 23) & 0x80000000u, mxy = (info << 22) & 0x80000000u,
+                   mxz = (info << 21) & 0x80000000u, myz = (info << 20) & 0x80000000u;
+    {
+      double2 T0 = lds_f64x2(ta), T1 = lds_f64x2(ta + 512), T2 = lds_f64x2(ta + 1024);
+      T0.y = xsign(T0.y, mc);
+      T1 = make_double2(xsign(T1.x, mxy), xsign(T1.y, mxy ^ mc));
+      T2 = make_double2(xsign(T2.x, mxz), xsign(T2.y, mxz ^ mc));
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (D::ok(t) && ((pm >> (4 * t + D::cp(t))) & 1u)) {
+          const int c = D::ok(t) ? D::cp(t) : 0;
+          cmac(acc[t][0], T0, U[c][0]);
+          cmac(acc[t][0], T1, U[c][KML > 1 ? 1 : 0]);
+          cmac(acc[t][0], T2, U[c][KML > 2 ? 2 : 0]);
+          cmac(acc[t][KML > 1 ? 1 : 0], T1, U[c][0]);
+          cmac(acc[t][KML > 2 ? 2 : 0], T2, U[c][0]);
+        }
+    }
+    {
+      double2 T3 = lds_f64x2(ta + 1536), T4 = lds_f64x2(ta + 2048), T5 = lds_f64x2(ta + 2560);
+      T3.y = xsign(T3.y, mc);
+      T5.y = xsign(T5.y, mc);
+      T4 = make_double2(xsign(T4.x, myz), xsign(T4.y, myz ^ mc));
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (D::ok(t) && ((pm >> (4 * t + D::cp(t))) & 1u)) {
+          const int c = D::ok(t) ? D::cp(t) : 0;
+          cmac(acc[t][KML > 1 ? 1 : 0], T3, U[c][KML > 1 ? 1 : 0]);
+          cmac(acc[t][KML > 1 ? 1 : 0], T4, U[c][KML > 2 ? 2 : 0]);
+          cmac(acc[t][KML > 2 ? 2 : 0], T4, U[c][KML > 1 ? 1 : 0]);
+          cmac(acc[t][KML > 2 ? 2 : 0], T5, U[c][KML > 2 ? 2 : 0]);
+        }
+    }
+    return;
+  }
+  double2 T[KML == 1 ? 1 : 6];
+  load_T<KML>(T, info, sT32, slots4);
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+    if (D::ok(t) && ((pm >> (4 * t + D::cp(t))) & 1u)) apply_T<KML>(acc[t], T, U[D::ok(t) ? D::cp(t) : 0]);
+}
+
+// 12 warps (<= 170 registers: 4 sources + 4 accumulators + the operator, no spills); 16
+// warps at 128 registers spill and measured slower (C5 product 557 vs 500 ms)
+#ifndef KF_GROUP_WARPS
+#define KF_GROUP_WARPS 12
+#endif
+#ifndef KF_GPF_L1
+#define KF_GPF_L1 0
+#endif
+constexpr int GROUP_WARPS = KF_GROUP_WARPS;
+
+template <int KML>
+__global__ void __launch_bounds__(GROUP_WARPS * 32, 1)
+    k_m2l_groups(int64_t nq, int NFP, int nrange, const double2* __restrict__ tbase, const int* __restrict__ rslot,
+                 const double2* __restrict__ ub, double2* __restrict__ cb, const int32_t* __restrict__ ioff,
+                 const int2* __restrict__ items, const uint8_t* __restrict__ tpat, const int32_t* __restrict__ wrange,
+                 const int32_t* __restrict__ ord) {
+  constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
+  extern __shared__ __align__(16) double2 sTb[];  // [N_BASE][NC][32]
+  const int g = blockIdx.y;
+  {
+    const double4* src = reinterpret_cast<const double4*>(tbase + (int64_t)g * N_BASE * NC * 32);
+    double4* dst = reinterpret_cast<double4*>(sTb);
+    for (int i = threadIdx.x; i < N_BASE * NC * 16; i += GROUP_WARPS * 32) dst[i] = src[i];
+  }
+  __syncthreads();
+  unsigned sT32;
+  asm volatile("mov.u32 %0, %1;" : "=r"(sT32) : "r"((unsigned)__cvta_generic_to_shared(sTb)));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned slots4;
+  {
+    const int rs = rslot[g * 32 + lane];
+    slots4 = (rs & 31) | (((rs >> 5) & 31) << 8) | (((rs >> 10) & 31) << 16) | (((rs >> 15) & 31) << 24);
+  }
+  const double2* ubg = ub + (int64_t)g * nq * R * 32 + lane;
+  const int r = blockIdx.x * GROUP_WARPS + warp;
+  if (r >= nrange) return;
+  const int pa = wrange[r], pe = wrange[r + 1];
+  int pb = pa;
+  int pend = ioff[min(pb + lane + 1, pe)];
+  auto unit_pat = [&](int id) { return ((unsigned)tpat[id >> 1] >> (4 * (id & 1))) & 15u; };
+  int pid = pb + lane < pe ? ord[pb + lane] : 0;
+  unsigned ppat = pb + lane < pe ? unit_pat(pid) : 0u;
+  const int ibeg = ioff[pa], iend = ioff[pe];
+  int ib = ibeg;  // lane l holds groups ib + l (bat) and ib + 32 + l (batn)
+  int2 bat = ib + lane < iend ? items[ib + lane] : make_int2(0, 0);
+  int2 batn = ib + 32 + lane < iend ? items[ib + 32 + lane] : make_int2(0, 0);
+  double2 acc[4][KML];
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+#pragma unroll
+    for (int a = 0; a < KML; ++a) acc[b][a] = make_double2(0.0, 0.0);
+  int P = pa;
+  int h = 0;  // x bit of the current unit's target children
+  int pcur_end = __shfl_sync(0xffffffffu, pend, 0);
+  auto flush = [&]() {
+    const unsigned bm = __shfl_sync(0xffffffffu, ppat, P - pb);
+    const int id = __shfl_sync(0xffffffffu, pid, P - pb);
+    double2* o = cb + ((int64_t)(id >> 1) * R + 4 * h * KML) * NFP + g * 32 + lane;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if ((bm >> b) & 1u) {
+#pragma unroll
+        for (int a = 0; a < KML; ++a) o[(int64_t)(b * KML + a) * NFP] = acc[b][a];
+      }
+#pragma unroll
+      for (int a = 0; a < KML; ++a) acc[b][a] = make_double2(0.0, 0.0);
+    }
+    ++P;
+    if (P < pe && P - pb == 32) {
+      pb = P;
+      pend = ioff[min(pb + lane + 1, pe)];
+      pid = pb + lane < pe ? ord[pb + lane] : 0;
+      ppat = pb + lane < pe ? unit_pat(pid) : 0u;
+    }
+    if (P < pe) {
+      pcur_end = __shfl_sync(0xffffffffu, pend, P - pb);
+      h = __shfl_sync(0xffffffffu, pid, P - pb) & 1;
+    }
+  };
+  h = __shfl_sync(0xffffffffu, pid, 0) & 1;
+  // the spectra rows of a group: 4 children x KML rows of 512 B = 4 x KML x 4 lines
+  auto prefetch = [&](int j) {
+    const int k = j - ib;
+    const int2 src = k < 32 ? bat : batn;
+    const int off = __shfl_sync(0xffffffffu, src.x, k & 31);
+    const unsigned sm = ((unsigned)__shfl_sync(0xffffffffu, src.y, k & 31) >> 22) & 15u;
+    constexpr int LPC = KML * 4;  // 128-B lines per child
+#pragma unroll
+    for (int s = 0; s < (4 * LPC + 31) / 32; ++s) {
+      const int l = lane + 32 * s;
+      if (l < 4 * LPC && ((sm >> (l / LPC)) & 1u))
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(ubg - lane + off + l * 8));
+    }
+  };
+  for (int j = ibeg; j < ibeg + ITEM_PF && j < iend; ++j) prefetch(j);
+  for (int i = ibeg; i < iend; ++i) {
+    while (i == pcur_end) flush();
+    if (i - ib == 32) {
+      ib = i;
+      bat = batn;
+      batn = ib + 32 + lane < iend ? items[ib + 32 + lane] : make_int2(0, 0);
+    }
+    const int off = __shfl_sync(0xffffffffu, bat.x, i - ib);
+    const unsigned y = (unsigned)__shfl_sync(0xffffffffu, bat.y, i - ib);
+    if (i + ITEM_PF < iend) prefetch(i + ITEM_PF);
+    double2 U[4][KML];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if ((y >> (22 + c)) & 1u) {  // absent children: no pair bit reads U[c]
+#pragma unroll
+        for (int e = 0; e < KML; ++e) U[c][e] = ubg[off + (c * KML + e) * 32];
+      }
+    }
+#if KF_GPF_L1
+    if (i + 1 < iend) {  // the next group's spectra into L1 (in flight during this group)
+      const int k = i + 1 - ib;
+      const int2 src = k < 32 ? bat : batn;
+      const int offn = __shfl_sync(0xffffffffu, src.x, k & 31);
+      const unsigned smn = ((unsigned)__shfl_sync(0xffffffffu, src.y, k & 31) >> 22) & 15u;
+      constexpr int LPC = KML * 4;
+#pragma unroll
+      for (int s = 0; s < (4 * LPC + 31) / 32; ++s) {
+        const int l = lane + 32 * s;
+        if (l < 4 * LPC && ((smn >> (l / LPC)) & 1u))
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(ubg - lane + offn + l * 8));
+      }
+    }
+#endif
+    const unsigned pm = (y >> 6) & 0xFFFFu;
+    const uint16_t* inf = c_pinfo + (y & 31u) * 64 + h * 32 + ((y >> 5) & 1u) * 4;
+    group_delta<KML, 0, 0>(acc, U, pm, inf, sT32, slots4);
+    group_delta<KML, 0, 1>(acc, U, pm, inf, sT32, slots4);
+    group_delta<KML, 0, -1>(acc, U, pm, inf, sT32, slots4);
+    group_delta<KML, 1, 0>(acc, U, pm, inf, sT32, slots4);
+    group_delta<KML, -1, 0>(acc, U, pm, inf, sT32, slots4);
+    group_delta<KML, 1, 1>(acc, U, pm, inf, sT32, slots4);
+    group_delta<KML, 1, -1>(acc, U, pm, inf, sT32, slots4);
+    group_delta<KML, -1, 1>(acc, U, pm, inf, sT32, slots4);
+    group_delta<KML, -1, -1>(acc, U, pm, inf, sT32, slots4);
+  }
+  while (P < pe) flush();
+}
+
 // base table of the sparse product: tbase[g][ob][c][s] = That_{o(ob)}(f(g, s))[c] (0 on padding slots)
 __global__ void k_tbase(int nfg, int nc, const int32_t* __restrict__ gfreq, const int16_t* __restrict__ boff,
                         const double2* __restrict__ that, double2* __restrict__ tbase) {
@@ -912,6 +1179,14 @@ int item_nb() {
   return v;
 }
 
+// sparse-chunk product: k_m2l_groups (operator reuse across the pairs of one offset;
+// default) or k_m2l_items (KAFMM_SPARSE=items, one operator load per pair).  Read at plan
+// setup (the stream layout differs) and stored in the chunk.
+bool sparse_groups() {
+  const char* e = getenv("KAFMM_SPARSE");
+  return !(e && std::string(e) == "items");
+}
+
 void run_m2l_fft(Plan& Pl) {
   for (const FftChunk& ch : Pl.fft_chunks) {
     if (ch.nt == 0 || ch.nq == 0) continue;
@@ -933,21 +1208,41 @@ void run_m2l_fft(Plan& Pl) {
             KF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(N_BASE * 6 * 32 * sizeof(double2))));
         }
-        const int nb = item_nb();
-        const int wpc = nb == 8 ? ItemCfg<8>::WARPS : ItemCfg<4>::WARPS;
-        const dim3 grid((unsigned)std::max<int64_t>(1, (ch.nrange + wpc - 1) / wpc), (unsigned)Pl.NFG);
+        if (ch.groups) {
+          static std::atomic<uint64_t> attr3{0};
+          if (first_on_device(attr3)) {
+            KF_CUDA(cudaFuncSetAttribute(k_m2l_groups<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(N_BASE * 32 * sizeof(double2))));
+            KF_CUDA(cudaFuncSetAttribute(k_m2l_groups<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(N_BASE * 6 * 32 * sizeof(double2))));
+          }
+          const dim3 grid((unsigned)std::max<int64_t>(1, (ch.nrange + GROUP_WARPS - 1) / GROUP_WARPS),
+                          (unsigned)Pl.NFG);
+          if (Pl.kml == 1)
+            k_m2l_groups<1><<<grid, GROUP_WARPS * 32, smem, Pl.stream>>>(
+                ch.nq, Pl.NFP, (int)ch.nrange, Pl.d_tbase, Pl.d_rslot, Pl.d_ub, Pl.d_cb, ch.d_ioff, ch.d_items,
+                ch.d_tpat, ch.d_wrange, ch.d_ord);
+          else
+            k_m2l_groups<3><<<grid, GROUP_WARPS * 32, smem, Pl.stream>>>(
+                ch.nq, Pl.NFP, (int)ch.nrange, Pl.d_tbase, Pl.d_rslot, Pl.d_ub, Pl.d_cb, ch.d_ioff, ch.d_items,
+                ch.d_tpat, ch.d_wrange, ch.d_ord);
+        } else {
+          const int nb = item_nb();
+          const int wpc = nb == 8 ? ItemCfg<8>::WARPS : ItemCfg<4>::WARPS;
+          const dim3 grid((unsigned)std::max<int64_t>(1, (ch.nrange + wpc - 1) / wpc), (unsigned)Pl.NFG);
 #define KF_ITEMS(KML, NB)                                                                                      \
   k_m2l_items<KML, NB><<<grid, wpc * 32, smem, Pl.stream>>>(ch.npar, ch.nq, Pl.NFP, (int)ch.nrange, Pl.d_tbase, \
                                                            Pl.d_rslot, Pl.d_ub, Pl.d_cb, ch.d_ioff, ch.d_items,  \
                                                            ch.d_tpat, ch.d_wrange, ch.d_ord)
-        if (Pl.kml == 1) {
-          if (nb == 8) KF_ITEMS(1, 8);
-          else KF_ITEMS(1, 4);
-        } else {
-          if (nb == 8) KF_ITEMS(3, 8);
-          else KF_ITEMS(3, 4);
-        }
+          if (Pl.kml == 1) {
+            if (nb == 8) KF_ITEMS(1, 8);
+            else KF_ITEMS(1, 4);
+          } else {
+            if (nb == 8) KF_ITEMS(3, 8);
+            else KF_ITEMS(3, 4);
+          }
 #undef KF_ITEMS
+        }
       }
     } else {
       // parent n-tiles per warp: NT_L / NT_G by default, KAFMM_DMMA_NT=<half> halves them
@@ -1428,9 +1723,10 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         // round-robin to W warps per frequency group (W = warps per CTA x CTAs per group, >= 4
         // units per warp), warp slot s taking unit positions s, s + W, s + 2W, ...; ord / ioff /
         // items follow that order, wrange cuts it per warp
-        const int nbu = item_nb(), halves = nbu == 8 ? 1 : 2;
+        const bool grp = sparse_groups();
+        const int nbu = grp ? 4 : item_nb(), halves = nbu == 8 ? 1 : 2;
         const int64_t nunit = ch.npar * halves;
-        const int64_t wpc = nbu == 8 ? ItemCfg<8>::WARPS : ItemCfg<4>::WARPS;
+        const int64_t wpc = grp ? GROUP_WARPS : nbu == 8 ? ItemCfg<8>::WARPS : ItemCfg<4>::WARPS;
         const int64_t X = std::min<int64_t>(148, std::max<int64_t>(1, (nunit + wpc * 4 - 1) / (wpc * 4)));
         const int64_t W = X * wpc;
         std::vector<int32_t> ord, ioff(1, 0), wr(1, 0);
@@ -1442,6 +1738,27 @@ void build_fft_chunks(Plan& P, int64_t budget) {
             const int64_t q = u / halves;
             const int h = (int)(u % halves);
             ord.push_back((int32_t)(halves == 1 ? q : 2 * q + h));
+            if (grp) {  // groups (unit, d, cx) of k_m2l_groups; items arrive in (d, c) order
+              int2 cur = make_int2(0, -1);
+              for (int64_t e = start[q]; e < start[q + 1]; ++e) {
+                const unsigned y = (unsigned)all[e].y;
+                const unsigned vm = ((y >> 11) >> (4 * h)) & 15u;
+                if (!vm) continue;
+                const unsigned dd = (y & 2047u) >> 6, c = y & 7u, cx = c >> 2, cq = c & 3u;
+                const unsigned key = dd | (cx << 5);
+                if (cur.y < 0 || ((unsigned)cur.y & 63u) != key) {
+                  if (cur.y >= 0) items.push_back(cur);
+                  cur = make_int2(all[e].x - (int)(cq * P.kml * 32), (int)key);
+                }
+                unsigned pm = 0;
+                for (int t = 0; t < 4; ++t)
+                  if ((vm >> t) & 1u) pm |= 1u << (4 * t + cq);
+                cur.y = (int)((unsigned)cur.y | (pm << 6) | (1u << (22 + cq)));
+              }
+              if (cur.y >= 0) items.push_back(cur);
+              ioff.push_back((int32_t)items.size());
+              continue;
+            }
             for (int64_t e = start[q]; e < start[q + 1]; ++e) {
               int2 it = all[e];
               if (halves == 2) {
@@ -1456,6 +1773,7 @@ void build_fft_chunks(Plan& P, int64_t budget) {
           wr.push_back((int32_t)ord.size());
         }
         ch.nitems = (int64_t)items.size();
+        ch.groups = grp;
         ch.nrange = W;
         ch.d_ioff = dalloc<int32_t>(P, ioff.size());
         ch.d_ord = dalloc<int32_t>(P, std::max<size_t>(1, ord.size()));

@@ -80,7 +80,8 @@ struct FftChunk {
   // CSR over the units in processing order
   int32_t* d_ioff = nullptr;    // units + 1
   int2* d_items = nullptr;      // {spectra block offset, item word: d*64+c | vmask << 11 | r << 19 | S << 29}
-  int64_t nitems = 0;
+  int64_t nitems = 0;           // items, or groups (unit, d, cx) when groups
+  bool groups = false;          // stream built for k_m2l_groups
   int64_t nsrc_children = 0;    // existing children of the chunk's source parents
   int32_t* d_ord = nullptr;     // units: processing order (parent id, or 2 parent + half)
   int32_t* d_wrange = nullptr;  // nrange + 1: each warp's positions in that order

@@ -43,3 +43,9 @@ for r in data:
         if k in h:
             i = h.index(k)
             print(f"   {name:22s} {r[i]:>18s} {units[i]}")
+    # warp stall reasons (cycles per issued instruction), the largest first
+    st = [(float(r[i] or 0), h[i]) for i in range(len(h))
+          if h[i].startswith("smsp__average_warps_issue_stalled_") and h[i].endswith("_per_issue_active.ratio")]
+    for v, k in sorted(st, reverse=True)[:8]:
+        if v >= 0.05:
+            print(f"   stall {k[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]:16s} {v:10.3f}")

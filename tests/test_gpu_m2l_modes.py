@@ -48,3 +48,26 @@ def test_m2l_variants_agree(case):
         for lo, hi in F.blocks(kernel):
             assert F.rel_l2(out[:, lo:hi], res["dense"][:, lo:hi]) < 1e-12, mode
         assert_parity(kernel, out, ref)
+
+
+@pytest.mark.parametrize("case", [CASES[0], CASES[2], CASES[5]], ids=["stokeslet", "rpy_spheres", "regvelomega"])
+def test_sparse_products_agree(case, monkeypatch):
+    """k_m2l_groups (operator loaded once per offset of a (unit, colleague, x half) group)
+    and k_m2l_items (once per V pair) on every FFT chunk: same products, so rounding-level
+    agreement, and both match the oracle (KAFMM_SPARSE is read at plan setup)."""
+    import torch
+    kernel, mk, p, cap = case
+    pts = mk()
+    vals = WL.random_values(kernel, pts.shape[0], 43)
+    src = torch.from_numpy(vals).cuda()
+    res = {}
+    for mode in ("items", "groups"):
+        monkeypatch.setenv("KAFMM_SPARSE", mode)
+        plan = KAFMM(pts, kernel, p, cap)
+        plan.set_m2l("fft_pairs")
+        res[mode] = plan.eval(src).cpu().numpy()
+        plan.close()
+    ref = F.fmm(pts, vals, kernel, p, cap)["out"]
+    for lo, hi in F.blocks(kernel):
+        assert F.rel_l2(res["groups"][:, lo:hi], res["items"][:, lo:hi]) < 1e-12
+    assert_parity(kernel, res["groups"], ref)
