@@ -389,8 +389,9 @@ def main():
                 f"{n_v_local} V pairs = {m2l_flop:.3e} flop")
         kname = ("m2l product: k_m2l_dmma (dense chunks: per-frequency complex GEMM over parent blocks, "
                  "DMMA.8x8x4, 3 real products per complex multiply-add = 6 of the 8 algorithmic flops) + "
-                 "k_m2l_items (sparse chunks: per-warp stream of (colleague, source child) items over half "
-                 "parents and 32 bins, absent child pairs skipped, on the DFMA pipe)")
+                 "k_m2l_groups (sparse chunks: per-warp stream of (half parent, colleague, source x half) "
+                 "groups over 32 bins, each offset's operator loaded once for its valid pairs, absent child "
+                 "pairs skipped, on the DFMA pipe; KAFMM_SPARSE=items selects the per-pair k_m2l_items)")
     else:
         m2l_flop = 2.0 * n * n * n_v_local
         algo = f"dense M2L: 2 n^2 flop per V pair, n={n}, {n_v_local} pairs = {m2l_flop:.3e} flop"

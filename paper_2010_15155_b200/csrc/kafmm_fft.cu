@@ -26,6 +26,7 @@
 #include <cufft.h>
 
 #include <algorithm>
+#include <numeric>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -545,6 +546,15 @@ __global__ void __launch_bounds__(DM_WARPS * 32, KML == 1 ? KF_DMMA_MINB1 : KF_D
 constexpr int N_BASE = 56;
 constexpr int SP_WARPS = 12;  // 384 threads, one CTA per SM (172 KB table), <= 170 registers
 __constant__ uint16_t c_pinfo[26 * 64];
+// c_grow[row], row = (dd * 2 + h) * 2 + cx: what k_m2l_groups needs per group, loaded once
+// in the group header (the offset 2d + c - b of a group's pairs depends only on the row
+// and delta = (cy - ty, cz - tz), index DL = 3 (DY + 1) + DZ + 1).  12 words:
+//   0-4  nine 16-bit fields f(DL) = base offset index << 5 | 8 x reflection r;
+//   5    SX (sign-bit mask: o_x < 0);  6, 7  SY for DY >= 0 / DY < 0;  8, 9  SZ likewise;
+//   10, 11  SX ^ SZ likewise.
+// The sign flips of an offset are 3-input XORs of these: conj = SZ, xy = SX ^ SY,
+// xy ^ conj = (SX ^ SZ) ^ SY, xz = SX ^ SZ, xz ^ conj = SX, yz = SY ^ SZ, yz ^ conj = SY.
+__constant__ uint4 c_grow[26 * 2 * 2 * 3];
 
 __device__ __forceinline__ double xsign(double v, unsigned m) {  // flip the sign bit if m = 0x80000000
   return __hiloint2double(__double2hiint(v) ^ (int)m, __double2loint(v));
@@ -817,52 +827,19 @@ __global__ void __launch_bounds__(ItemCfg<NB>::WARPS * 32, 1)
 // FP64 pipe, bounds it.  But the offset o = 2d + c - b of a child pair depends only on
 // c - b within one colleague: in a half-parent unit (target children b = 4h + t, t =
 // (ty, tz)) and one x half cx of colleague Q_d (source children c = 4cx + c', c' = (cy, cz)),
-// the 16 pairs (t, c') share 9 offsets, indexed by (cy - ty, cz - tz).  A group =
+// the 16 pairs (t, c') share 9 offsets, indexed by delta = (cy - ty, cz - tz).  A group =
 // (unit, d, cx) with its 16-bit pair mask: the lane holds the 4 source spectra and the
 // 4 accumulators, and each offset's T is loaded once for all the valid pairs that use
-// it (full 4 x 4 blocks: 9 loads per 16 pairs).  Group word y: bits 0-4 the direction
-// slot dd, bit 5 cx, bits 6-21 the pair mask (bit 4t + c'), bits 22-25 the source mask.
-// Signs and reflection per offset come from c_pinfo (S [conj] T_|o|(R f) S).
-template <int KML>
-__device__ __forceinline__ void load_T(double2 (&T)[KML == 1 ? 1 : 6], unsigned info, unsigned sT32,
-                                       unsigned slots4) {
-  constexpr unsigned OB = (KML == 1 ? 1 : 6) * 32 * 16;
-  const unsigned t = sT32 + __byte_perm(slots4, 0u, ((info >> 6) & 3u) | 0x4440u) * 16u + (info & 63u) * OB;
-  const unsigned mc = (info << 23) & 0x80000000u;
-  if (KML == 1) {
-    T[0] = lds_f64x2(t);
-    T[0].y = xsign(T[0].y, mc);
-  } else {
-#pragma unroll
-    for (int k = 0; k < 6; ++k) T[k] = lds_f64x2(t + k * 32 * 16);
-    const unsigned mxy = (info << 22) & 0x80000000u, mxz = (info << 21) & 0x80000000u,
-                   myz = (info << 20) & 0x80000000u;
-    T[0].y = xsign(T[0].y, mc);
-    T[3].y = xsign(T[3].y, mc);
-    T[5].y = xsign(T[5].y, mc);
-    T[1] = make_double2(xsign(T[1].x, mxy), xsign(T[1].y, mxy ^ mc));
-    T[2] = make_double2(xsign(T[2].x, mxz), xsign(T[2].y, mxz ^ mc));
-    T[4] = make_double2(xsign(T[4].x, myz), xsign(T[4].y, myz ^ mc));
-  }
-}
-
-template <int KML>
-__device__ __forceinline__ void apply_T(double2 (&o)[KML], const double2 (&T)[KML == 1 ? 1 : 6],
-                                        const double2 (&U)[KML]) {
-  if (KML == 1) {
-    cmac(o[0], T[0], U[0]);
-  } else {
-    cmac(o[0], T[0], U[0]);
-    cmac(o[0], T[1], U[KML > 1 ? 1 : 0]);
-    cmac(o[0], T[2], U[KML > 2 ? 2 : 0]);
-    cmac(o[KML > 1 ? 1 : 0], T[1], U[0]);
-    cmac(o[KML > 1 ? 1 : 0], T[3], U[KML > 1 ? 1 : 0]);
-    cmac(o[KML > 1 ? 1 : 0], T[4], U[KML > 2 ? 2 : 0]);
-    cmac(o[KML > 2 ? 2 : 0], T[2], U[0]);
-    cmac(o[KML > 2 ? 2 : 0], T[4], U[KML > 1 ? 1 : 0]);
-    cmac(o[KML > 2 ? 2 : 0], T[5], U[KML > 2 ? 2 : 0]);
-  }
-}
+// it (full 4 x 4 blocks: 9 loads per 16 pairs).  Group word y: bits 0-6 the c_grow row
+// (dd * 2 + h) * 2 + cx, bits 7-22 the pair mask (bit 4t + c'), bits 23-26 the source mask.
+//
+// Everything that steers a group is warp-uniform, and the kernel tells the compiler so:
+// the group word goes through a ballot (lane l contributes bit l; a ballot is uniform by
+// construction), so the pair tests compile to plain branches without BSSY / BSYNC
+// reconvergence pairs, and each offset's table address, reflection selector and sign
+// masks (S [conj] T_|o|(R f) S) derive from the group's c_grow row, loaded once per group
+// (ncu, C5 level 9, before: 42.6% of the warp instructions were DFMA, 15.4% branch
+// bookkeeping, 18% LOP3).
 
 // pairs (t, c') of one offset delta = (cy - ty, cz - tz), DY, DZ in {-1, 0, 1}
 template <int DY, int DZ>
@@ -875,63 +852,71 @@ struct GDelta {
     return (ok(0) ? 1u << cp(0) : 0u) | (ok(1) ? 1u << (4 + cp(1)) : 0u) | (ok(2) ? 1u << (8 + cp(2)) : 0u) |
            (ok(3) ? 1u << (12 + cp(3)) : 0u);
   }
-  static constexpr int t0() { return ok(0) ? 0 : ok(1) ? 1 : ok(2) ? 2 : 3; }
 };
 
-#ifndef KF_TSPLIT
-#define KF_TSPLIT 1
-#endif
+__device__ __forceinline__ double xsign2(double v, unsigned m1, unsigned m2) {  // one LOP3
+  return __hiloint2double(__double2hiint(v) ^ (int)m1 ^ (int)m2, __double2loint(v));
+}
+
+// the group's row of c_grow in registers
+struct GRow {
+  unsigned w[5], sx, sy[2], sz[2], sxz[2];
+};
+
+// one offset of a group: load T once (Stokes family: in two halves, T0..T2 then T3..T5,
+// 12 registers live instead of 24), apply it to every valid pair of the delta.  The
+// table address comes from the row's field by a few fixed-latency integer operations (a
+// constant load per offset put ~70 cycles ahead of every T load: ncu, C5 level 9).
 template <int KML, int DY, int DZ>
 __device__ __forceinline__ void group_delta(double2 (&acc)[4][KML], const double2 (&U)[4][KML], unsigned pm,
-                                            const uint16_t* inf, unsigned sT32, unsigned slots4) {
+                                            const GRow& g, unsigned sT32, unsigned slots4) {
   using D = GDelta<DY, DZ>;
   if (!(pm & D::mask())) return;
-  const unsigned info = inf[D::t0() * 8 + D::cp(D::t0())];
-  if (KML == 3 && KF_TSPLIT) {
-    // the operator in two halves (T0..T2, then T3..T5): 12 registers live instead of 24,
-    // so 4 sources + 4 accumulators + T fit 128 registers (16 warps per SM)
-    constexpr unsigned OB = 6 * 32 * 16;
-    const unsigned ta = sT32 + __byte_perm(slots4, 0u, ((info >> 6) & 3u) | 0x4440u) * 16u + (info & 63u) * OB;
-    const unsigned mc = (info << 23) & 0x80000000u, mxy = (info << 22) & 0x80000000u,
-                   mxz = (info << 21) & 0x80000000u, myz = (info << 20) & 0x80000000u;
-    {
-      double2 T0 = lds_f64x2(ta), T1 = lds_f64x2(ta + 512), T2 = lds_f64x2(ta + 1024);
-      T0.y = xsign(T0.y, mc);
-      T1 = make_double2(xsign(T1.x, mxy), xsign(T1.y, mxy ^ mc));
-      T2 = make_double2(xsign(T2.x, mxz), xsign(T2.y, mxz ^ mc));
+  constexpr int DL = 3 * (DY + 1) + DZ + 1;
+  constexpr unsigned OB32 = (KML == 1 ? 1 : 6) * 16;  // operator bytes / 32
+  const unsigned f = (DL & 1) ? g.w[DL / 2] >> 16 : g.w[DL / 2];  // bits 16.. of an even field: masked below
+  const unsigned slot = (slots4 >> (f & 31u)) & 0xFFu;
+  const unsigned ta = (f & 0xFFE0u) * OB32 + sT32 + slot * 16u;
+  const unsigned SY = g.sy[DY < 0], SZ = g.sz[DZ < 0], SXZ = g.sxz[DZ < 0];
+  if (KML == 1) {
+    double2 T0 = lds_f64x2(ta);
+    T0.y = xsign(T0.y, SZ);
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (D::ok(t) && ((pm >> (4 * t + D::cp(t))) & 1u)) {
-          const int c = D::ok(t) ? D::cp(t) : 0;
-          cmac(acc[t][0], T0, U[c][0]);
-          cmac(acc[t][0], T1, U[c][KML > 1 ? 1 : 0]);
-          cmac(acc[t][0], T2, U[c][KML > 2 ? 2 : 0]);
-          cmac(acc[t][KML > 1 ? 1 : 0], T1, U[c][0]);
-          cmac(acc[t][KML > 2 ? 2 : 0], T2, U[c][0]);
-        }
-    }
-    {
-      double2 T3 = lds_f64x2(ta + 1536), T4 = lds_f64x2(ta + 2048), T5 = lds_f64x2(ta + 2560);
-      T3.y = xsign(T3.y, mc);
-      T5.y = xsign(T5.y, mc);
-      T4 = make_double2(xsign(T4.x, myz), xsign(T4.y, myz ^ mc));
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (D::ok(t) && ((pm >> (4 * t + D::cp(t))) & 1u)) {
-          const int c = D::ok(t) ? D::cp(t) : 0;
-          cmac(acc[t][KML > 1 ? 1 : 0], T3, U[c][KML > 1 ? 1 : 0]);
-          cmac(acc[t][KML > 1 ? 1 : 0], T4, U[c][KML > 2 ? 2 : 0]);
-          cmac(acc[t][KML > 2 ? 2 : 0], T4, U[c][KML > 1 ? 1 : 0]);
-          cmac(acc[t][KML > 2 ? 2 : 0], T5, U[c][KML > 2 ? 2 : 0]);
-        }
-    }
+    for (int t = 0; t < 4; ++t)
+      if (D::ok(t) && ((pm >> (4 * t + D::cp(t))) & 1u)) cmac(acc[t][0], T0, U[D::ok(t) ? D::cp(t) : 0][0]);
     return;
   }
-  double2 T[KML == 1 ? 1 : 6];
-  load_T<KML>(T, info, sT32, slots4);
+  {
+    double2 T0 = lds_f64x2(ta), T1 = lds_f64x2(ta + 512), T2 = lds_f64x2(ta + 1024);
+    T0.y = xsign(T0.y, SZ);
+    T1 = make_double2(xsign2(T1.x, g.sx, SY), xsign2(T1.y, SXZ, SY));
+    T2 = make_double2(xsign(T2.x, SXZ), xsign(T2.y, g.sx));
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
-    if (D::ok(t) && ((pm >> (4 * t + D::cp(t))) & 1u)) apply_T<KML>(acc[t], T, U[D::ok(t) ? D::cp(t) : 0]);
+    for (int t = 0; t < 4; ++t)
+      if (D::ok(t) && ((pm >> (4 * t + D::cp(t))) & 1u)) {
+        const int c = D::ok(t) ? D::cp(t) : 0;
+        cmac(acc[t][0], T0, U[c][0]);
+        cmac(acc[t][0], T1, U[c][KML > 1 ? 1 : 0]);
+        cmac(acc[t][0], T2, U[c][KML > 2 ? 2 : 0]);
+        cmac(acc[t][KML > 1 ? 1 : 0], T1, U[c][0]);
+        cmac(acc[t][KML > 2 ? 2 : 0], T2, U[c][0]);
+      }
+  }
+  {
+    double2 T3 = lds_f64x2(ta + 1536), T4 = lds_f64x2(ta + 2048), T5 = lds_f64x2(ta + 2560);
+    T3.y = xsign(T3.y, SZ);
+    T5.y = xsign(T5.y, SZ);
+    T4 = make_double2(xsign2(T4.x, SY, SZ), xsign(T4.y, SY));
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (D::ok(t) && ((pm >> (4 * t + D::cp(t))) & 1u)) {
+        const int c = D::ok(t) ? D::cp(t) : 0;
+        cmac(acc[t][KML > 1 ? 1 : 0], T3, U[c][KML > 1 ? 1 : 0]);
+        cmac(acc[t][KML > 1 ? 1 : 0], T4, U[c][KML > 2 ? 2 : 0]);
+        cmac(acc[t][KML > 2 ? 2 : 0], T4, U[c][KML > 1 ? 1 : 0]);
+        cmac(acc[t][KML > 2 ? 2 : 0], T5, U[c][KML > 2 ? 2 : 0]);
+      }
+  }
 }
 
 // 12 warps (<= 170 registers: 4 sources + 4 accumulators + the operator, no spills); 16
@@ -939,25 +924,28 @@ __device__ __forceinline__ void group_delta(double2 (&acc)[4][KML], const double
 #ifndef KF_GROUP_WARPS
 #define KF_GROUP_WARPS 12
 #endif
-#ifndef KF_GPF_L1
-#define KF_GPF_L1 0
+#ifndef KF_GROUP_CHUNK
+#define KF_GROUP_CHUNK 4
 #endif
 constexpr int GROUP_WARPS = KF_GROUP_WARPS;
+constexpr int GROUP_CHUNK = KF_GROUP_CHUNK;  // unit positions per dynamically taken range
 
 template <int KML>
 __global__ void __launch_bounds__(GROUP_WARPS * 32, 1)
-    k_m2l_groups(int64_t nq, int NFP, int nrange, const double2* __restrict__ tbase, const int* __restrict__ rslot,
+    k_m2l_groups(int64_t nq, int NFP, int nper, const double2* __restrict__ tbase, const int* __restrict__ rslot,
                  const double2* __restrict__ ub, double2* __restrict__ cb, const int32_t* __restrict__ ioff,
                  const int2* __restrict__ items, const uint8_t* __restrict__ tpat, const int32_t* __restrict__ wrange,
                  const int32_t* __restrict__ ord) {
   constexpr int NC = KML == 1 ? 1 : 6, R = 8 * KML;
   extern __shared__ __align__(16) double2 sTb[];  // [N_BASE][NC][32]
+  __shared__ int s_next;  // the CTA's next untaken range
   const int g = blockIdx.y;
   {
     const double4* src = reinterpret_cast<const double4*>(tbase + (int64_t)g * N_BASE * NC * 32);
     double4* dst = reinterpret_cast<double4*>(sTb);
     for (int i = threadIdx.x; i < N_BASE * NC * 16; i += GROUP_WARPS * 32) dst[i] = src[i];
   }
+  if (threadIdx.x == 0) s_next = GROUP_WARPS;  // ranges 0 .. GROUP_WARPS - 1 go to the warps directly
   __syncthreads();
   unsigned sT32;
   asm volatile("mov.u32 %0, %1;" : "=r"(sT32) : "r"((unsigned)__cvta_generic_to_shared(sTb)));
@@ -967,9 +955,9 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32, 1)
     const int rs = rslot[g * 32 + lane];
     slots4 = (rs & 31) | (((rs >> 5) & 31) << 8) | (((rs >> 10) & 31) << 16) | (((rs >> 15) & 31) << 24);
   }
-  const double2* ubg = ub + (int64_t)g * nq * R * 32 + lane;
-  const int r = blockIdx.x * GROUP_WARPS + warp;
-  if (r >= nrange) return;
+  const double2* ubg = ub + (int64_t)g * nq * R * 32;  // the frequency group's spectra rows
+  for (int rc = warp; rc < nper;) {
+  const int r = blockIdx.x * nper + rc;
   const int pa = wrange[r], pe = wrange[r + 1];
   int pb = pa;
   int pend = ioff[min(pb + lane + 1, pe)];
@@ -1014,21 +1002,22 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32, 1)
     }
   };
   h = __shfl_sync(0xffffffffu, pid, 0) & 1;
-  // the spectra rows of a group: 4 children x KML rows of 512 B = 4 x KML x 4 lines
-  auto prefetch = [&](int j) {
-    const int k = j - ib;
-    const int2 src = k < 32 ? bat : batn;
-    const int off = __shfl_sync(0xffffffffu, src.x, k & 31);
-    const unsigned sm = ((unsigned)__shfl_sync(0xffffffffu, src.y, k & 31) >> 22) & 15u;
-    constexpr int LPC = KML * 4;  // 128-B lines per child
+  // L2 prefetch of a group's spectra rows (4 children x KML rows of 512 B = 4 x KML x 4
+  // lines, the present children only): the warp's first 32 groups up front, then group
+  // i + 32 while group i is processed -- it sits in batn at the lane group i has in bat,
+  // so one lane index serves both broadcasts
+  constexpr int LPC = KML * 4;  // 128-B lines per child
+  auto prefetch = [&](int off, unsigned sm) {
+    const double2* pl = ubg + (off + lane * 8);  // lane l: line l (and l + 32)
 #pragma unroll
     for (int s = 0; s < (4 * LPC + 31) / 32; ++s) {
       const int l = lane + 32 * s;
-      if (l < 4 * LPC && ((sm >> (l / LPC)) & 1u))
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(ubg - lane + off + l * 8));
+      if (l < 4 * LPC && ((sm >> (l / LPC)) & 1u)) asm volatile("prefetch.global.L2 [%0];" ::"l"(pl + s * 256));
     }
   };
-  for (int j = ibeg; j < ibeg + ITEM_PF && j < iend; ++j) prefetch(j);
+#pragma unroll 1
+  for (int j = 0; j < 32 && ibeg + j < iend; ++j)
+    prefetch(__shfl_sync(0xffffffffu, bat.x, j), ((unsigned)__shfl_sync(0xffffffffu, bat.y, j) >> 23) & 15u);
   for (int i = ibeg; i < iend; ++i) {
     while (i == pcur_end) flush();
     if (i - ib == 32) {
@@ -1036,45 +1025,47 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32, 1)
       bat = batn;
       batn = ib + 32 + lane < iend ? items[ib + 32 + lane] : make_int2(0, 0);
     }
-    const int off = __shfl_sync(0xffffffffu, bat.x, i - ib);
-    const unsigned y = (unsigned)__shfl_sync(0xffffffffu, bat.y, i - ib);
-    if (i + ITEM_PF < iend) prefetch(i + ITEM_PF);
+    const int k = i - ib;
+    const int off = __shfl_sync(0xffffffffu, bat.x, k);
+    const unsigned y = (unsigned)__shfl_sync(0xffffffffu, bat.y, k);
+    // past the end batn holds zeros: an empty source mask, nothing prefetched
+    prefetch(__shfl_sync(0xffffffffu, batn.x, k), ((unsigned)__shfl_sync(0xffffffffu, batn.y, k) >> 23) & 15u);
     double2 U[4][KML];
+    const double2* pu = ubg + (off + lane);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      if ((y >> (22 + c)) & 1u) {  // absent children: no pair bit reads U[c]
+      if ((y >> (23 + c)) & 1u) {  // absent children: no pair bit reads U[c]
 #pragma unroll
-        for (int e = 0; e < KML; ++e) U[c][e] = ubg[off + (c * KML + e) * 32];
+        for (int e = 0; e < KML; ++e) U[c][e] = pu[(c * KML + e) * 32];
       }
     }
-#if KF_GPF_L1
-    if (i + 1 < iend) {  // the next group's spectra into L1 (in flight during this group)
-      const int k = i + 1 - ib;
-      const int2 src = k < 32 ? bat : batn;
-      const int offn = __shfl_sync(0xffffffffu, src.x, k & 31);
-      const unsigned smn = ((unsigned)__shfl_sync(0xffffffffu, src.y, k & 31) >> 22) & 15u;
-      constexpr int LPC = KML * 4;
-#pragma unroll
-      for (int s = 0; s < (4 * LPC + 31) / 32; ++s) {
-        const int l = lane + 32 * s;
-        if (l < 4 * LPC && ((smn >> (l / LPC)) & 1u))
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(ubg - lane + offn + l * 8));
-      }
+    const unsigned yu = __ballot_sync(0xffffffffu, (y >> lane) & 1u);  // = y, known uniform
+    const unsigned pm = (yu >> 7) & 0xFFFFu;
+    GRow gi;
+    {
+      const uint4* gr = c_grow + (yu & 127u) * 3;
+      const uint4 q0 = gr[0], q1 = gr[1], q2 = gr[2];
+      gi.w[0] = q0.x, gi.w[1] = q0.y, gi.w[2] = q0.z, gi.w[3] = q0.w, gi.w[4] = q1.x;
+      gi.sx = q1.y, gi.sy[0] = q1.z, gi.sy[1] = q1.w;
+      gi.sz[0] = q2.x, gi.sz[1] = q2.y, gi.sxz[0] = q2.z, gi.sxz[1] = q2.w;
     }
-#endif
-    const unsigned pm = (y >> 6) & 0xFFFFu;
-    const uint16_t* inf = c_pinfo + (y & 31u) * 64 + h * 32 + ((y >> 5) & 1u) * 4;
-    group_delta<KML, 0, 0>(acc, U, pm, inf, sT32, slots4);
-    group_delta<KML, 0, 1>(acc, U, pm, inf, sT32, slots4);
-    group_delta<KML, 0, -1>(acc, U, pm, inf, sT32, slots4);
-    group_delta<KML, 1, 0>(acc, U, pm, inf, sT32, slots4);
-    group_delta<KML, -1, 0>(acc, U, pm, inf, sT32, slots4);
-    group_delta<KML, 1, 1>(acc, U, pm, inf, sT32, slots4);
-    group_delta<KML, 1, -1>(acc, U, pm, inf, sT32, slots4);
-    group_delta<KML, -1, 1>(acc, U, pm, inf, sT32, slots4);
-    group_delta<KML, -1, -1>(acc, U, pm, inf, sT32, slots4);
+    group_delta<KML, 0, 0>(acc, U, pm, gi, sT32, slots4);
+    group_delta<KML, 0, 1>(acc, U, pm, gi, sT32, slots4);
+    group_delta<KML, 0, -1>(acc, U, pm, gi, sT32, slots4);
+    group_delta<KML, 1, 0>(acc, U, pm, gi, sT32, slots4);
+    group_delta<KML, -1, 0>(acc, U, pm, gi, sT32, slots4);
+    group_delta<KML, 1, 1>(acc, U, pm, gi, sT32, slots4);
+    group_delta<KML, 1, -1>(acc, U, pm, gi, sT32, slots4);
+    group_delta<KML, -1, 1>(acc, U, pm, gi, sT32, slots4);
+    group_delta<KML, -1, -1>(acc, U, pm, gi, sT32, slots4);
   }
   while (P < pe) flush();
+  {
+    int nx = 0;
+    if (lane == 0) nx = atomicAdd(&s_next, 1);
+    rc = __shfl_sync(0xffffffffu, nx, 0);
+  }
+  }
 }
 
 // base table of the sparse product: tbase[g][ob][c][s] = That_{o(ob)}(f(g, s))[c] (0 on padding slots)
@@ -1186,7 +1177,6 @@ bool sparse_groups() {
   const char* e = getenv("KAFMM_SPARSE");
   return !(e && std::string(e) == "items");
 }
-
 void run_m2l_fft(Plan& Pl) {
   for (const FftChunk& ch : Pl.fft_chunks) {
     if (ch.nt == 0 || ch.nq == 0) continue;
@@ -1216,15 +1206,14 @@ void run_m2l_fft(Plan& Pl) {
             KF_CUDA(cudaFuncSetAttribute(k_m2l_groups<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(N_BASE * 6 * 32 * sizeof(double2))));
           }
-          const dim3 grid((unsigned)std::max<int64_t>(1, (ch.nrange + GROUP_WARPS - 1) / GROUP_WARPS),
-                          (unsigned)Pl.NFG);
+          const dim3 grid((unsigned)std::max<int64_t>(1, ch.nrange / std::max<int64_t>(1, ch.nper)), (unsigned)Pl.NFG);
           if (Pl.kml == 1)
             k_m2l_groups<1><<<grid, GROUP_WARPS * 32, smem, Pl.stream>>>(
-                ch.nq, Pl.NFP, (int)ch.nrange, Pl.d_tbase, Pl.d_rslot, Pl.d_ub, Pl.d_cb, ch.d_ioff, ch.d_items,
+                ch.nq, Pl.NFP, (int)ch.nper, Pl.d_tbase, Pl.d_rslot, Pl.d_ub, Pl.d_cb, ch.d_ioff, ch.d_items,
                 ch.d_tpat, ch.d_wrange, ch.d_ord);
           else
             k_m2l_groups<3><<<grid, GROUP_WARPS * 32, smem, Pl.stream>>>(
-                ch.nq, Pl.NFP, (int)ch.nrange, Pl.d_tbase, Pl.d_rslot, Pl.d_ub, Pl.d_cb, ch.d_ioff, ch.d_items,
+                ch.nq, Pl.NFP, (int)ch.nper, Pl.d_tbase, Pl.d_rslot, Pl.d_ub, Pl.d_cb, ch.d_ioff, ch.d_items,
                 ch.d_tpat, ch.d_wrange, ch.d_ord);
         } else {
           const int nb = item_nb();
@@ -1363,6 +1352,31 @@ static void build_sparse_tables(Plan& P, const int16_t* tab) {
       }
   }
   KF_CUDA(cudaMemcpyToSymbolAsync(c_pinfo, info.data(), info.size() * 2, 0, cudaMemcpyHostToDevice, st));
+  {
+    std::vector<uint32_t> gr(26 * 2 * 2 * 12, 0u);
+    for (int dd = 0; dd < 26; ++dd)
+      for (int h = 0; h < 2; ++h)
+        for (int cx = 0; cx < 2; ++cx) {
+          uint32_t* e = &gr[((size_t)(dd * 2 + h) * 2 + cx) * 12];
+          const int d = dd < 13 ? dd : dd + 1;
+          const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
+          const uint32_t S = 0x80000000u;
+          const int ox = 2 * dx + cx - h;
+          const uint32_t SX = ox < 0 ? S : 0, SYn = dy < 0 ? S : 0, SYm = dy <= 0 ? S : 0, SZn = dz < 0 ? S : 0,
+                         SZm = dz <= 0 ? S : 0;
+          e[5] = SX, e[6] = SYn, e[7] = SYm, e[8] = SZn, e[9] = SZm, e[10] = SX ^ SZn, e[11] = SX ^ SZm;
+          for (int dl = 0; dl < 9; ++dl) {
+            const int DY = dl / 3 - 1, DZ = dl % 3 - 1;
+            const int oy = 2 * dy + DY, oz = 2 * dz + DZ;
+            if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) < 2) continue;  // adjacent: never used
+            const int sx = ox < 0, sy = oy < 0, sz = oz < 0;
+            const int ob = bidx[std::abs(ox) * 16 + std::abs(oy) * 4 + std::abs(oz)];
+            const int r = (sx ^ sz) | ((sy ^ sz) << 1);
+            e[dl / 2] |= (uint32_t)((ob << 5) | (8 * r)) << (16 * (dl % 2));
+          }
+        }
+    KF_CUDA(cudaMemcpyToSymbolAsync(c_grow, gr.data(), gr.size() * 4, 0, cudaMemcpyHostToDevice, st));
+  }
   P.d_fpos = dalloc<int16_t>(P, NF);
   P.d_rslot = dalloc<int>(P, P.NFP);
   KF_CUDA(cudaMemcpyAsync(P.d_fpos, fpos.data(), NF * 2, cudaMemcpyHostToDevice, st));
@@ -1733,8 +1747,22 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         std::vector<int2> items;
         ord.reserve(nunit);
         items.reserve(all.size() * halves);
-        for (int64_t sl = 0; sl < W; ++sl) {
-          for (int64_t u = sl; u < nunit; u += W) {
+        // k_m2l_groups takes its ranges dynamically: a range is GROUP_CHUNK (4; measured C5 product 8: 431, 4: 425, 16: 435 ms) consecutive
+        // positions of one slot, a CTA's ranges ordered chunk-major (all its slots' first
+        // chunk, then the second, ...) so that the warps of the whole grid still sweep the
+        // same window of Morton-adjacent parents; a warp that finishes early takes the next
+        // range of its CTA (ncu, C5 level 9, static ranges: 10.8 of 12 warps active on
+        // average, the sub-partitions idle 5% of the cycles).  k_m2l_items keeps one range per
+        // warp (chunk = all positions).
+        const int64_t npos = (nunit + W - 1) / W;
+        const int64_t cpos = grp ? GROUP_CHUNK : std::max<int64_t>(1, npos);
+        const int64_t nchunk = std::max<int64_t>(1, (npos + cpos - 1) / cpos);
+        for (int64_t rg = 0; rg < X * nchunk * wpc; ++rg) {
+          // range rg = (CTA x, chunk j, warp slot s) -> slot sl, positions [j cpos, (j + 1) cpos)
+          const int64_t x = rg / (nchunk * wpc), j = (rg / wpc) % nchunk, sl = x * wpc + rg % wpc;
+          for (int64_t pos = j * cpos; pos < std::min(npos, (j + 1) * cpos); ++pos) {
+            const int64_t u = pos * W + sl;
+            if (u >= nunit) continue;
             const int64_t q = u / halves;
             const int h = (int)(u % halves);
             ord.push_back((int32_t)(halves == 1 ? q : 2 * q + h));
@@ -1745,15 +1773,15 @@ void build_fft_chunks(Plan& P, int64_t budget) {
                 const unsigned vm = ((y >> 11) >> (4 * h)) & 15u;
                 if (!vm) continue;
                 const unsigned dd = (y & 2047u) >> 6, c = y & 7u, cx = c >> 2, cq = c & 3u;
-                const unsigned key = dd | (cx << 5);
-                if (cur.y < 0 || ((unsigned)cur.y & 63u) != key) {
+                const unsigned key = (dd * 2 + (unsigned)h) * 2 + cx;  // the c_grow row
+                if (cur.y < 0 || ((unsigned)cur.y & 127u) != key) {
                   if (cur.y >= 0) items.push_back(cur);
                   cur = make_int2(all[e].x - (int)(cq * P.kml * 32), (int)key);
                 }
                 unsigned pm = 0;
                 for (int t = 0; t < 4; ++t)
                   if ((vm >> t) & 1u) pm |= 1u << (4 * t + cq);
-                cur.y = (int)((unsigned)cur.y | (pm << 6) | (1u << (22 + cq)));
+                cur.y = (int)((unsigned)cur.y | (pm << 7) | (1u << (23 + cq)));
               }
               if (cur.y >= 0) items.push_back(cur);
               ioff.push_back((int32_t)items.size());
@@ -1774,7 +1802,8 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         }
         ch.nitems = (int64_t)items.size();
         ch.groups = grp;
-        ch.nrange = W;
+        ch.nrange = X * nchunk * wpc;
+        ch.nper = nchunk * wpc;
         ch.d_ioff = dalloc<int32_t>(P, ioff.size());
         ch.d_ord = dalloc<int32_t>(P, std::max<size_t>(1, ord.size()));
         ch.d_wrange = dalloc<int32_t>(P, wr.size());

@@ -86,6 +86,7 @@ struct FftChunk {
   int32_t* d_ord = nullptr;     // units: processing order (parent id, or 2 parent + half)
   int32_t* d_wrange = nullptr;  // nrange + 1: each warp's positions in that order
   int64_t nrange = 0;
+  int64_t nper = 0;             // ranges per CTA (k_m2l_groups takes them dynamically)
   double block_fill = 1.0;      // V pairs / (8x8 child blocks the DMMA product runs)
 };
 
