@@ -1177,6 +1177,13 @@ bool sparse_groups() {
   const char* e = getenv("KAFMM_SPARSE");
   return !(e && std::string(e) == "items");
 }
+// unit positions per dynamically taken range of k_m2l_groups (host-side layout only);
+// KAFMM_GROUP_CHUNK overrides (tests force 1 to get many ranges on small clouds)
+static int64_t group_chunk() {
+  const char* e = getenv("KAFMM_GROUP_CHUNK");
+  return e && atoi(e) > 0 ? atoi(e) : GROUP_CHUNK;
+}
+
 void run_m2l_fft(Plan& Pl) {
   for (const FftChunk& ch : Pl.fft_chunks) {
     if (ch.nt == 0 || ch.nq == 0) continue;
@@ -1755,7 +1762,7 @@ void build_fft_chunks(Plan& P, int64_t budget) {
         // average, the sub-partitions idle 5% of the cycles).  k_m2l_items keeps one range per
         // warp (chunk = all positions).
         const int64_t npos = (nunit + W - 1) / W;
-        const int64_t cpos = grp ? GROUP_CHUNK : std::max<int64_t>(1, npos);
+        const int64_t cpos = grp ? group_chunk() : std::max<int64_t>(1, npos);
         const int64_t nchunk = std::max<int64_t>(1, (npos + cpos - 1) / cpos);
         for (int64_t rg = 0; rg < X * nchunk * wpc; ++rg) {
           // range rg = (CTA x, chunk j, warp slot s) -> slot sl, positions [j cpos, (j + 1) cpos)

@@ -71,3 +71,29 @@ def test_sparse_products_agree(case, monkeypatch):
     for lo, hi in F.blocks(kernel):
         assert F.rel_l2(res["groups"][:, lo:hi], res["items"][:, lo:hi]) < 1e-12
     assert_parity(kernel, res["groups"], ref)
+
+
+@pytest.mark.parametrize("kernel,p", [("stokeslet", 6), ("laplace_pgrad", 5)])
+def test_groups_dynamic_ranges(kernel, p, monkeypatch):
+    """k_m2l_groups takes ranges of unit positions from a per-CTA counter; at test sizes a
+    warp slot has a single range, so KAFMM_GROUP_CHUNK=1 (one unit position per range)
+    forces dozens of dynamically taken ranges per CTA.  Same arithmetic per unit, so the
+    two layouts agree to rounding (M2M accumulates with atomics: not bitwise), and match
+    the oracle."""
+    import torch
+    pts = WL.make_points(WL.CONFIGS[5], 30000, n_spheres=12)
+    vals = WL.random_values(kernel, pts.shape[0], 47)
+    src = torch.from_numpy(vals).cuda()
+    res = {}
+    for ck in ("1", "64"):
+        monkeypatch.setenv("KAFMM_GROUP_CHUNK", ck)
+        plan = KAFMM(pts, kernel, p, 40)
+        plan.set_m2l("fft_pairs")
+        res[ck] = plan.eval(src).cpu().numpy()
+        st = plan.fft_stats()
+        plan.close()
+    assert st["items"] > 0
+    for lo, hi in F.blocks(kernel):
+        assert F.rel_l2(res["1"][:, lo:hi], res["64"][:, lo:hi]) < 1e-12
+    ref = F.fmm(pts, vals, kernel, p, 40)["out"]
+    assert_parity(kernel, res["1"], ref)
